@@ -1,0 +1,151 @@
+"""Seeded, deterministic input generators and the BASELINE.json workload presets.
+
+This module holds NO arithmetic of the method (no sampling, no estimator, no Hamiltonian):
+only query grids (inclusive linspace, row-major, last axis fastest, R21), fixed
+coordinates of the slices (R15, R16), the Philox seeds, and the configuration numbers of the
+five BASELINE.json configs. It is the one module both the CUDA path's tests/bench and the
+oracle's tests use, so both sides see the identical fp32 query array.
+
+System / target names are strings; each side maps them to its own identifiers.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+import math
+
+import numpy as np
+
+SEED_BASE = 0x5EED000000000001  # seed = SEED_BASE + config index (0-based)
+
+
+@dataclass(frozen=True)
+class Preset:
+    """One workload: the problem definition plus how its query slice is laid out."""
+
+    name: str
+    n: int
+    delta: float
+    T: float
+    K: int
+    Kp: int
+    N: int
+    system: str
+    target: str
+    sys_params: tuple = ()
+    tgt_params: tuple = ()
+    visc: str = "paper"          # "paper" = (δ/2)Δ (R1), "full" = δΔ
+    crn: bool = True             # R10
+    antithetic: bool = False
+    m0: float = 1e-3
+    c_min: float = 0.05
+    c_max: float = 20.0
+    seed: int = SEED_BASE
+    tag: int = 0
+    # slice layout
+    grid_axes: tuple = (0, 1)    # which state coordinates vary over the 2-D grid
+    grid_lo: float = -1.0
+    grid_hi: float = 1.0
+    grid_pts: int = 64
+    fixed: tuple = ()            # full-state template (values of the non-grid coordinates)
+    slices: tuple = ((),)        # per-slice overrides: tuple of (coord, value) pairs
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def M(self) -> int:
+        return self.grid_pts * self.grid_pts * len(self.slices)
+
+    @property
+    def evals(self) -> int:
+        """query·sample evaluations of the whole workload (the metric's unit count)."""
+        return self.M * self.N * self.K * self.Kp
+
+    def with_(self, **kw) -> "Preset":
+        return replace(self, **kw)
+
+
+def grid_2d(lo: float, hi: float, pts: int) -> tuple[np.ndarray, np.ndarray]:
+    """Inclusive linspace on both axes, row-major (first axis slow, second fast)."""
+    ax = np.linspace(lo, hi, pts, dtype=np.float64)
+    a, b = np.meshgrid(ax, ax, indexing="ij")
+    return a.reshape(-1), b.reshape(-1)
+
+
+def queries(p: Preset) -> np.ndarray:
+    """The fp32 query array x[M][n] of a preset (all slices concatenated, slice-major)."""
+    a, b = grid_2d(p.grid_lo, p.grid_hi, p.grid_pts)
+    blocks = []
+    for sl in p.slices:
+        x = np.zeros((a.size, p.n), dtype=np.float64)
+        if p.fixed:
+            x[:] = np.asarray(p.fixed, dtype=np.float64)[None, :]
+        for coord, val in sl:
+            x[:, coord] = val
+        x[:, p.grid_axes[0]] = a
+        x[:, p.grid_axes[1]] = b
+        blocks.append(x)
+    return np.ascontiguousarray(np.concatenate(blocks, axis=0).astype(np.float32))
+
+
+def pair_fixed(K: int, theta1: float) -> tuple:
+    """R16: pair 0 is the slice's free pair (heading theta1); pair q ≥ 1 sits off-target at
+    (10 + 2q, 0) with heading 0."""
+    s = [0.0] * (3 * K)
+    s[2] = theta1
+    for q in range(1, K):
+        s[3 * q] = 10.0 + 2.0 * q
+    return tuple(s)
+
+
+# ---- the five BASELINE.json configs --------------------------------
+C1 = Preset(
+    name="c1_quadratic_n2", n=2, delta=0.05, T=0.5, K=1, Kp=1, N=4096,
+    system="quadratic", target="quad_bowl", tgt_params=(0.25,),
+    grid_lo=-1.0, grid_hi=1.0, grid_pts=64, seed=SEED_BASE + 0,
+)
+C2 = Preset(
+    name="c2_dubins_n3", n=3, delta=0.01, T=1.0, K=10, Kp=8, N=65536,
+    system="dubins_rel", target="disk", sys_params=(5.0, 5.0, 1.0), tgt_params=(5.0,),
+    grid_lo=-20.0, grid_hi=20.0, grid_pts=101, fixed=(0.0, 0.0, math.pi / 2),
+    seed=SEED_BASE + 1,
+)
+C3 = Preset(
+    name="c3_rocket6_n6", n=6, delta=0.01, T=1.0, K=10, Kp=8, N=1 << 18,
+    system="rocket6", target="rel_disk6", sys_params=(64.0, 32.0, 1.0), tgt_params=(1.5,),
+    grid_lo=-20.0, grid_hi=20.0, grid_pts=201, fixed=(0.0,) * 6, seed=SEED_BASE + 2,
+)
+C4 = Preset(
+    name="c4_dubins5pairs_n15", n=15, delta=0.01, T=1.0, K=10, Kp=10, N=1 << 20,
+    system="dubins_pairs", target="pair_union", sys_params=(5.0, 5.0, 1.0), tgt_params=(1.0,),
+    grid_lo=-20.0, grid_hi=20.0, grid_pts=201, fixed=pair_fixed(5, math.pi / 2),
+    seed=SEED_BASE + 3,
+)
+C5 = Preset(
+    name="c5_dubins15pairs_n45", n=45, delta=0.01, T=1.0, K=10, Kp=10, N=1 << 20,
+    system="dubins_pairs", target="pair_union", sys_params=(5.0, 5.0, 1.0), tgt_params=(1.0,),
+    grid_lo=-20.0, grid_hi=20.0, grid_pts=256, fixed=pair_fixed(15, 0.0),
+    slices=tuple(((2, k * math.pi / 4),) for k in range(8)), seed=SEED_BASE + 4,
+)
+# The paper's own Dubins slice settings (40×40, N=14,000, δ=0.08), unit speeds
+# (P:1263–1267), capture radius 1 — a context preset only (Table 2's 24.9 s per slice).
+PAPER_DUBINS = Preset(
+    name="paper_dubins_40x40", n=3, delta=0.08, T=1.0, K=1, Kp=15, N=14000,
+    system="dubins_rel", target="disk", sys_params=(1.0, 1.0, 1.0), tgt_params=(1.0,),
+    grid_lo=-5.0, grid_hi=5.0, grid_pts=40, fixed=(0.0, 0.0, 0.0), seed=SEED_BASE + 5,
+)
+
+PRESETS = {p.name: p for p in (C1, C2, C3, C4, C5, PAPER_DUBINS)}
+BY_INDEX = {1: C1, 2: C2, 3: C3, 4: C4, 5: C5}
+
+
+def subsample_ids(M: int, count: int, seed: int = 12345) -> np.ndarray:
+    """Deterministic spread of `count` query ids over [0, M) (parity / oracle-timing samples)."""
+    if count >= M:
+        return np.arange(M, dtype=np.int64)
+    base = np.linspace(0, M - 1, count).round().astype(np.int64)
+    return np.unique(base)
+
+
+def random_queries(n: int, M: int, lo: float, hi: float, seed: int) -> np.ndarray:
+    """Seeded uniform random fp32 queries (used for ragged / edge-case parity inputs)."""
+    rng = np.random.default_rng(seed)
+    return rng.uniform(lo, hi, size=(M, n)).astype(np.float32)

@@ -1,0 +1,206 @@
+"""Pins of the oracle's Hamiltonians, coefficient map Γ, Picard driver, tube and residuals.
+
+H: worked cases derived by hand from the paper's formulas (S:122–123 for Dubins; R15 for the
+6-D rocket game), positive 1-homogeneity of the game Hamiltonians, and the C2-slice
+identity H = −5(x+y)/r at θ = π/2 with p = Dg.
+Γ: the exact Cole–Hopf case c = 1/δ_eff; floor and clamp.
+Picard: quadratic + common random numbers is exactly stationary; tube ≤ g and ≤ every
+horizon's value; the per-sample BRT band bound; determinism across thread counts and shards.
+"""
+import math
+
+import numpy as np
+import pytest
+
+
+def test_dubins_spec_cases(oracle_mod):
+    O = oracle_mod
+    P = O.Problem(n=3, system="dubins_rel", sys_params=(1.0, 1.0, 1.0))
+    assert O.hamiltonian(P, (0, 0, 0), (1, 0, 0)) == 0.0
+    assert O.hamiltonian(P, (0, 0, 0), (0, 0, 1)) == 0.0
+    assert O.hamiltonian(P, (3, -2, 1), (0, 0, 0)) == 0.0
+    # x3 = π: p1 (cos π − 1) = −2 p1 with unit speeds, the turn terms cancel at x = 0, p3 = 0
+    assert abs(O.hamiltonian(P, (0, 0, math.pi), (1, 0, 0)) - (-2.0)) < 1e-15
+
+
+def test_dubins_c2_slice_identity(oracle_mod):
+    """At θ = π/2, v_p = v_e = 5, w = 1 and p = Dg = (x, y, 0)/r:
+    H = −5x/r − 5y/r + |x y/r − y x/r| = −5(x+y)/r, so c_raw = −1000 (x+y)/r at δ = 0.01."""
+    O = oracle_mod
+    P = O.Problem(n=3, delta=0.01, system="dubins_rel", sys_params=(5.0, 5.0, 1.0),
+                  target="disk", tgt_params=(5.0,), c_min=-1e9, c_max=1e9)
+    for x, y in ((3.0, 4.0), (-7.0, 2.0), (0.4, -0.4), (12.0, 12.0)):
+        r = math.hypot(x, y)
+        p = O.dg(P, (x, y, math.pi / 2))
+        assert abs(O.hamiltonian(P, (x, y, math.pi / 2), p) - (-5 * (x + y) / r)) < 1e-12
+        assert abs(O.gamma(P, (x, y, math.pi / 2), p) - (-1000 * (x + y) / r)) < 1e-8
+
+
+def test_rocket6_hand_cases(oracle_mod):
+    O = oracle_mod
+    P = O.Problem(n=6, system="rocket6", sys_params=(64.0, 32.0, 1.0))
+    x0 = np.zeros(6)
+    e = np.eye(6)
+    assert O.hamiltonian(P, x0, e[0]) == 64.0      # a cos 0
+    assert O.hamiltonian(P, x0, e[1]) == -32.0     # a sin 0 − g
+    assert O.hamiltonian(P, x0, e[2]) == -1.0      # −|p_θP|
+    assert O.hamiltonian(P, x0, e[3]) == 65.0      # a + d_max
+    assert O.hamiltonian(P, x0, e[4]) == -31.0     # −g + d_max
+    assert O.hamiltonian(P, x0, e[5]) == 1.0       # +|p_θE|
+    xs = np.array([0, 0, math.pi / 2, 0, 0, 0])
+    assert abs(O.hamiltonian(P, xs, e[1]) - 32.0) < 1e-12   # a sin(π/2) − g
+
+
+@pytest.mark.parametrize("system,n", [("dubins_rel", 3), ("rocket6", 6), ("dubins_pairs", 15)])
+def test_game_hamiltonian_positive_homogeneity(oracle_mod, system, n):
+    O = oracle_mod
+    P = O.Problem(n=n, system=system)
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        x, p = rng.normal(size=n) * 3, rng.normal(size=n)
+        h = O.hamiltonian(P, x, p)
+        for lam in (0.1, 2.5, 40.0):
+            assert abs(O.hamiltonian(P, x, lam * p) - lam * h) < 1e-9 * max(1, abs(lam * h))
+
+
+def test_dubins_pairs_is_sum_of_pairs(oracle_mod):
+    O = oracle_mod
+    P3 = O.Problem(n=3, system="dubins_rel")
+    P9 = O.Problem(n=9, system="dubins_pairs")
+    rng = np.random.default_rng(2)
+    x, p = rng.normal(size=9), rng.normal(size=9)
+    s = sum(O.hamiltonian(P3, x[3 * q:3 * q + 3], p[3 * q:3 * q + 3]) for q in range(3))
+    assert abs(O.hamiltonian(P9, x, p) - s) < 1e-12
+
+
+@pytest.mark.parametrize("visc", ["paper", "full"])
+def test_gamma_quadratic_exact(oracle_mod, visc):
+    """H = |p|²/2 ⇒ c = 2H/(δ|p|²) = 1/δ_eff for every p ≠ 0."""
+    O = oracle_mod
+    P = O.Problem(n=3, delta=0.1, visc=visc)
+    rng = np.random.default_rng(4)
+    for _ in range(20):
+        p = rng.normal(size=3) * rng.uniform(1e-4, 10)
+        assert abs(O.gamma(P, np.zeros(3), p) - 1.0 / P.delta_eff) < 1e-12
+    assert abs(O.gamma(P, np.zeros(3), np.zeros(3)) - 1.0 / P.delta_eff) < 1e-12  # p = 0 → m0 e1
+
+
+def test_gamma_floor_and_clamp(oracle_mod):
+    O = oracle_mod
+    # rocket-style negative H at δ = 0.08 clamps to c_min
+    P = O.Problem(n=6, delta=0.08, system="rocket6")
+    assert O.gamma(P, np.zeros(6), np.eye(6)[4]) == P.c_min
+    assert O.gamma(P, np.zeros(6), np.eye(6)[0]) == P.c_max      # 2·64/0.08 = 1600 → c_max
+    # floor: |p| < m0 is scaled up to m0 (1-homogeneous H ⇒ c ∝ 1/|p̃|)
+    P = O.Problem(n=3, delta=0.01, system="dubins_rel", c_min=-1e12, c_max=1e12)
+    x = np.array([1.0, 2.0, 0.3])
+    p = np.array([1e-5, 0.0, 0.0])
+    assert abs(O.gamma(P, x, p) - O.gamma(P, x, p / 1e-5 * 1e-3)) < 1e-6
+    assert math.isfinite(O.gamma(P, x, np.zeros(3)))
+
+
+def _quad_problem(O, **kw):
+    d = dict(n=2, delta=0.05, T=0.5, K=3, Kp=3, N=2000, system="quadratic", target="quad_bowl",
+             tgt_params=(0.25,))
+    d.update(kw)
+    return O.Problem(**d)
+
+
+def test_picard_quadratic_crn_stationary(oracle_mod):
+    """c never moves for H = |p|²/2, so with common random numbers v^(2) = v^(1)."""
+    O = oracle_mod
+    P = _quad_problem(O)
+    x = np.random.default_rng(0).uniform(-1, 1, (20, 2)).astype(np.float32)
+    r = O.solve_slice(P, x)
+    assert r["status"] == 0
+    for k in range(1, P.Kp):
+        assert np.abs(r["vhist"][:, k] - r["vhist"][:, 0]).max() <= 1e-12
+    assert np.abs(r["chist"] - 1 / P.delta).max() <= 1e-12
+    # without CRN the iterates move by MC noise only
+    r2 = O.solve_slice(_quad_problem(O, crn=False), x)
+    assert np.abs(r2["vhist"][:, 1] - r2["vhist"][:, 0]).max() > 1e-8
+
+
+def test_picard_matches_phi_gamma_composition(oracle_mod):
+    """solve_slice is exactly the composition Γ∘Φ of Algorithm 1 (checked step by step)."""
+    O = oracle_mod
+    P = O.Problem(n=3, delta=0.01, T=1.0, K=2, Kp=3, N=1500, system="dubins_rel",
+                  target="disk", tgt_params=(5.0,))
+    x = np.array([[4.0, 3.5, 1.0], [-6.0, 1.0, 0.2]], dtype=np.float32)
+    r = O.solve_slice(P, x, qid_base=40)
+    for m in range(2):
+        xm = x[m].astype(np.float64)
+        for j in (1, 2):
+            c = O.gamma(P, xm, O.dg(P, xm))
+            for k in range(P.Kp):
+                v, dv, _, _ = O.phi(P, xm, c, j * P.T / P.K, qid=40 + m, jw=j, kw=0)
+                assert r["chist"][j - 1, k, m] == c
+                assert r["vhist"][j - 1, k, m] == v
+                c = O.gamma(P, xm, dv)
+        assert r["c"][m] == c
+
+
+def test_tube_properties_and_brt_band(oracle_mod):
+    O = oracle_mod
+    P = O.Problem(n=3, delta=0.01, T=1.0, K=4, Kp=2, N=3000, system="dubins_rel",
+                  target="disk", tgt_params=(5.0,))
+    a = np.linspace(-12, 12, 9)
+    X, Y = np.meshgrid(a, a, indexing="ij")
+    x = np.stack([X.ravel(), Y.ravel(), np.full(X.size, math.pi / 2)], 1).astype(np.float32)
+    r = O.solve_slice(P, x)
+    assert np.all(r["tube"] <= r["g0"])
+    assert np.all(r["tube"] <= r["vhist"][:, -1, :].min(0))
+    assert np.all((r["tube"] == r["g0"]) | (r["tube"] == r["vhist"][:, -1, :].min(0)))
+    # v̂ ≥ min_i g(y_i) ≥ g(x) − σ_K max‖(z0, z1)‖ (g 1-Lipschitz), ‖(z0,z1)‖ ≤ sqrt(48 ln 2)
+    sigma_K = math.sqrt(P.delta * P.T)
+    band = sigma_K * math.sqrt(48 * math.log(2))
+    inside = r["tube"] <= 0
+    assert np.all(r["g0"][inside] <= band)
+
+
+def test_determinism_threads_and_shards(oracle_mod):
+    O = oracle_mod
+    P = O.Problem(n=3, delta=0.01, T=1.0, K=2, Kp=2, N=800, system="dubins_rel",
+                  target="disk", tgt_params=(5.0,))
+    x = np.random.default_rng(5).uniform(-8, 8, (13, 3)).astype(np.float32)
+    full = O.solve_slice(P, x, nthreads=1)
+    par = O.solve_slice(P, x, nthreads=4)
+    a = O.solve_slice(P, x[:6], qid_base=0)
+    b = O.solve_slice(P, x[6:], qid_base=6)
+    for key in ("v", "c", "tube"):
+        np.testing.assert_array_equal(full[key], par[key])
+        np.testing.assert_array_equal(full[key], np.concatenate([a[key], b[key]]))
+    np.testing.assert_array_equal(full["vhist"], np.concatenate([a["vhist"], b["vhist"]], axis=2))
+
+
+def test_residual_partials_hand(oracle_mod):
+    O = oracle_mod
+    vhist = np.array([[[1.0, 2.0], [1.5, 2.0]]])        # K=1, Kp=2, M=2
+    g0 = np.array([0.0, 1.0])
+    out = O.residual_partials(vhist, g0)
+    np.testing.assert_allclose(out[0, 0], [1.0 + 1.0, 0.0 + 1.0])
+    np.testing.assert_allclose(out[0, 1], [0.25, 1.0 + 4.0])
+
+
+def test_concentration_rate(oracle_mod):
+    """Thm 1 / P:365: the estimator error is O(N^-1/2): log-log slope of std over seeds."""
+    O = oracle_mod
+    Ns = [2**8, 2**9, 2**10, 2**11, 2**12]
+    stds = []
+    for N in Ns:
+        vals = []
+        for s in range(64):
+            P = O.Problem(n=2, delta=0.05, N=N, seed=1000 + s, target="quad_bowl", tgt_params=(0.25,))
+            v, _, _, _ = O.phi(P, (0.5, 0.5), 20.0, 0.5)
+            vals.append(v)
+        stds.append(np.std(vals, ddof=1))
+    slope = np.polyfit(np.log(Ns), np.log(stds), 1)[0]
+    assert abs(slope + 0.5) < 0.12
+
+
+def test_corollary1_sample_size():
+    """Cor. 1: N ≥ (β−α)²/(2α²(1−e^{−cε})²) log(2/α); S:222's example N ≈ 276."""
+    c, gmin, gmax, eps = 1.0, 0.0, 1.0, 0.1
+    alpha, beta = math.exp(-c * gmax), math.exp(-c * gmin)
+    N = (beta - alpha) ** 2 / (2 * alpha**2 * (1 - math.exp(-c * eps)) ** 2) * math.log(2 / alpha)
+    assert abs(N - 276.008) < 1e-3
