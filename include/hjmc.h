@@ -111,6 +111,12 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#define HJMC_API __attribute__((visibility("default")))
+#else
+#define HJMC_API
+#endif
+
 #define HJMC_VERSION_MAJOR 0
 #define HJMC_VERSION_MINOR 1
 
@@ -180,26 +186,26 @@ typedef struct hjmc_handle hjmc_handle;
 
 /* Fill *cfg with the defaults: n=2, δ=0.05, T=0.5, K=1, Kp=1, N=4096, seed=0x5EED000000000001,
  * paper convention, crn=1, antithetic=0, m0=1e−3, c_min=0.05, c_max=20, tag=0, device=0, flags=0. */
-void hjmc_config_defaults(hjmc_config* cfg);
+HJMC_API void hjmc_config_defaults(hjmc_config* cfg);
 
 /* Validate cfg (δ>0, T>0, 1≤n≤HJMC_MAX_N, K in 1..65535, Kp≥1 (≤256 if !crn), N≥1,
  * m0≥0, 0<c_min≤c_max, visc∈{0,1}) and create a handle on cfg->device.
  * Returns HJMC_EINVAL (no handle) or HJMC_ECUDA; *out is NULL on failure. */
-int hjmc_create(const hjmc_config* cfg, hjmc_handle** out);
+HJMC_API int hjmc_create(const hjmc_config* cfg, hjmc_handle** out);
 
 /* Release the handle's device scratch. Safe on NULL. Synchronises the device. */
-void hjmc_destroy(hjmc_handle* h);
+HJMC_API void hjmc_destroy(hjmc_handle* h);
 
 /* Select the Hamiltonian H (see SYSTEMS above). params: host pointer to np floats (np=0 →
  * defaults). HJMC_EINVAL if the id is unknown, np is wrong or n is incompatible. */
-int hjmc_set_dynamics(hjmc_handle* h, int32_t system_id, const float* params, int32_t np);
+HJMC_API int hjmc_set_dynamics(hjmc_handle* h, int32_t system_id, const float* params, int32_t np);
 
 /* Select the terminal cost g (see TARGETS above). HJMC_EUNSUPPORTED if no kernel exists for
  * (target, n); HJMC_EINVAL for a bad id / np / n. */
-int hjmc_set_target(hjmc_handle* h, int32_t target_id, const float* params, int32_t np);
+HJMC_API int hjmc_set_target(hjmc_handle* h, int32_t target_id, const float* params, int32_t np);
 
 /* 1 if a kernel for (target_id, n) is compiled in, else 0. */
-int hjmc_supported(int32_t target_id, int32_t n);
+HJMC_API int hjmc_supported(int32_t target_id, int32_t n);
 
 /* One Φ pass at frozen per-query coefficients (Thm 2's map Φ).
  *   x      dev [M][n]   query states
@@ -210,7 +216,7 @@ int hjmc_supported(int32_t target_id, int32_t n);
  *   drift  dev [M][n] or NULL (R4)
  *   v      dev [M] out;  dv dev [M][n] out or NULL
  * M = 0 is a no-op. Asynchronous on stream. */
-int hjmc_value_grad(hjmc_handle* h, const float* x, const float* c, const uint32_t* qid,
+HJMC_API int hjmc_value_grad(hjmc_handle* h, const float* x, const float* c, const uint32_t* qid,
                     uint32_t qid_base, int64_t M, float tau, uint32_t j_tag, uint32_t k_tag,
                     const float* drift, float* v, float* dv, void* stream);
 
@@ -218,49 +224,49 @@ int hjmc_value_grad(hjmc_handle* h, const float* x, const float* c, const uint32
  * running-min tube, for M queries, in one fused kernel plus a tube epilogue kernel.
  *   x dev [M][n]; qid / qid_base as in hjmc_value_grad; drift dev [M][n] or NULL.
  *   out: device pointers (each may be NULL). M = 0 is a no-op. Asynchronous on stream. */
-int hjmc_solve_slice(hjmc_handle* h, const float* x, const uint32_t* qid, uint32_t qid_base,
+HJMC_API int hjmc_solve_slice(hjmc_handle* h, const float* x, const uint32_t* qid, uint32_t qid_base,
                      int64_t M, const float* drift, const hjmc_result* out, void* stream);
 
 /* End-to-end convenience: the same solve with HOST buffers. Copies x (and drift) to handle-owned
  * device scratch, solves, copies the requested outputs back to the HOST pointers in *out_host,
  * and synchronises. Returns HJMC_ENUMERIC on a numerical failure. */
-int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, uint32_t qid_base, int64_t M,
+HJMC_API int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, uint32_t qid_base, int64_t M,
                           const float* drift_host, const hjmc_result* out_host);
 
 /* g(x) and the analytic Dg(x) used for c^(0) (dev pointers; dg may be NULL). */
-int hjmc_eval_target(hjmc_handle* h, const float* x, int64_t M, float* g, float* dg,
+HJMC_API int hjmc_eval_target(hjmc_handle* h, const float* x, int64_t M, float* g, float* dg,
                      void* stream);
 
 /* H(x, p) and Γ(x, p) per query (dev pointers; either output may be NULL). */
-int hjmc_eval_hamiltonian(hjmc_handle* h, const float* x, const float* p, int64_t M,
+HJMC_API int hjmc_eval_hamiltonian(hjmc_handle* h, const float* x, const float* p, int64_t M,
                           float* H, float* c, void* stream);
 
 /* The sampled normals exactly as the kernels generate them, for RNG parity tests:
  * z[s][n] (dev) for samples i = i0 .. i0+count−1 of query qid with counter tags (jw, kw);
  * raw[s][4·ceil(n/4)] (dev, may be NULL) receives the Philox words. Antithetic sign applies. */
-int hjmc_debug_normals(hjmc_handle* h, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
+HJMC_API int hjmc_debug_normals(hjmc_handle* h, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
                        uint32_t count, float* z, uint32_t* raw, void* stream);
 
 /* Synchronise stream, then return HJMC_ENUMERIC if any earlier call on this handle produced
  * a non-finite value (clearing the flag), else HJMC_OK. */
-int hjmc_check(hjmc_handle* h, void* stream);
+HJMC_API int hjmc_check(hjmc_handle* h, void* stream);
 
 /* Smallest global query id that failed numerically since the last hjmc_check, or −1. */
-int64_t hjmc_last_bad_query(const hjmc_handle* h);
+HJMC_API int64_t hjmc_last_bad_query(const hjmc_handle* h);
 
 /* Message of the last failure on this handle (or of the last failed hjmc_create if h is NULL). */
-const char* hjmc_last_error(const hjmc_handle* h);
+HJMC_API const char* hjmc_last_error(const hjmc_handle* h);
 
 /* Host-side Picard residual partial sums (a12; R11). For each (j, k):
  *   num[j][k] = Σ_m (v^(k+1)_m − v^(k)_m)²,  den[j][k] = Σ_m (v^(k)_m)²,
  * with v^(0) = g0 (Algorithm 1 init v^(0) = g) and v^(k+1) = vhist[j][k].
  * Host pointers: vhist [K][Kp][M], g0 [M], out [K][Kp][2] (num, den) in double.
  * ε_j(k) = sqrt(num/den) after summing partials over shards. */
-int hjmc_residual_partials(const float* vhist, const float* g0, int32_t K, int32_t Kp, int64_t M,
+HJMC_API int hjmc_residual_partials(const float* vhist, const float* g0, int32_t K, int32_t Kp, int64_t M,
                            double* out);
 
 /* Library version as MAJOR*1000 + MINOR. */
-int hjmc_version(void);
+HJMC_API int hjmc_version(void);
 
 #ifdef __cplusplus
 }

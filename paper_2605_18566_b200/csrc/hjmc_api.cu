@@ -1,0 +1,491 @@
+// hjmc_api.cu — the C-ABI of libhjmc (include/hjmc.h): validation, handle-owned scratch,
+// launch orchestration and error reporting. No C++ exception crosses the boundary.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/hjmc.h"
+#include "hjmc_kernels.cuh"
+
+using namespace hjmc;
+
+struct hjmc_handle {
+  hjmc_config cfg{};
+  bool sys_set = false;
+  bool tgt_set = false;
+  SystemParams sp{};
+  TargetParams tp{};
+  int tgt_id = -1;
+  KernelSet ks{};
+  int* d_err = nullptr;
+  unsigned long long* d_bad = nullptr;
+  float* d_g0 = nullptr;
+  size_t g0_cap = 0;
+  float* d_vfinal = nullptr;
+  size_t vfinal_cap = 0;
+  // host-path staging
+  float* d_stage = nullptr;
+  size_t stage_cap = 0;
+  cudaStream_t host_stream = nullptr;
+  int64_t last_bad = -1;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_create_error;
+
+int fail(hjmc_handle* h, int code, const std::string& msg) {
+  if (h) h->err = msg; else g_create_error = msg;
+  return code;
+}
+
+int cuda_fail(hjmc_handle* h, cudaError_t e, const char* where) {
+  return fail(h, HJMC_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+int ensure(hjmc_handle* h, float** buf, size_t* cap, size_t elems) {
+  if (elems <= *cap && *buf) return HJMC_OK;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMalloc((void**)buf, elems * sizeof(float));
+  if (e != cudaSuccess) {
+    *buf = nullptr;
+    return fail(h, HJMC_ENOMEM, std::string("scratch allocation failed: ") + cudaGetErrorString(e));
+  }
+  *cap = elems;
+  return HJMC_OK;
+}
+
+int set_device(hjmc_handle* h) {
+  cudaError_t e = cudaSetDevice(h->cfg.device);
+  return e == cudaSuccess ? HJMC_OK : cuda_fail(h, e, "cudaSetDevice");
+}
+
+double delta_eff(const hjmc_config& c) {
+  return c.visc == HJMC_VISC_FULL_LAPLACIAN ? 2.0 * (double)c.delta : (double)c.delta;
+}
+
+void fill_common(const hjmc_handle* h, SolveParams* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->N = h->cfg.N;
+  p->key.k0 = (uint32_t)(h->cfg.seed & 0xFFFFFFFFull);
+  p->key.k1 = (uint32_t)(h->cfg.seed >> 32);
+  p->tag = h->cfg.tag;
+  p->crn = h->cfg.crn;
+  p->antithetic = h->cfg.antithetic;
+  p->gp.delta_eff = delta_eff(h->cfg);
+  p->gp.m0 = h->cfg.m0;
+  p->gp.c_min = h->cfg.c_min;
+  p->gp.c_max = h->cfg.c_max;
+  p->sp = h->sp;
+  p->tp = h->tp;
+  p->err = h->d_err;
+  p->bad = h->d_bad;
+}
+
+int ready(hjmc_handle* h) {
+  if (!h) return HJMC_EINVAL;
+  if (!h->sys_set) return fail(h, HJMC_EINVAL, "hjmc_set_dynamics has not been called");
+  if (!h->tgt_set) return fail(h, HJMC_EINVAL, "hjmc_set_target has not been called");
+  return HJMC_OK;
+}
+
+int sync_check_if_requested(hjmc_handle* h, cudaStream_t s) {
+  if (h->cfg.flags & HJMC_FLAG_SYNC_CHECK) return hjmc_check(h, (void*)s);
+  return HJMC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void hjmc_config_defaults(hjmc_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->n = 2;
+  c->delta = 0.05f;
+  c->T = 0.5f;
+  c->K = 1;
+  c->Kp = 1;
+  c->N = 4096;
+  c->seed = 0x5EED000000000001ull;
+  c->visc = HJMC_VISC_PAPER_HALF_LAPLACIAN;
+  c->crn = 1;
+  c->antithetic = 0;
+  c->m0 = 1e-3f;
+  c->c_min = 0.05f;
+  c->c_max = 20.0f;
+  c->tag = 0;
+  c->device = 0;
+  c->flags = 0;
+}
+
+int hjmc_version(void) { return HJMC_VERSION_MAJOR * 1000 + HJMC_VERSION_MINOR; }
+
+int hjmc_create(const hjmc_config* cfg, hjmc_handle** out) {
+  if (!out) return fail(nullptr, HJMC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(nullptr, HJMC_EINVAL, "cfg is NULL");
+  const hjmc_config& c = *cfg;
+  if (c.n < 1 || c.n > HJMC_MAX_N) return fail(nullptr, HJMC_EINVAL, "n must be in 1..64");
+  if (!(c.delta > 0.f) || !std::isfinite(c.delta)) return fail(nullptr, HJMC_EINVAL, "delta must be > 0");
+  if (!(c.T > 0.f) || !std::isfinite(c.T)) return fail(nullptr, HJMC_EINVAL, "T must be > 0");
+  if (c.K < 1 || c.K > 65535) return fail(nullptr, HJMC_EINVAL, "K must be in 1..65535");
+  if (c.Kp < 1) return fail(nullptr, HJMC_EINVAL, "Kp must be >= 1");
+  if (!c.crn && c.Kp > 256) return fail(nullptr, HJMC_EINVAL, "Kp must be <= 256 without crn");
+  if (c.N < 1) return fail(nullptr, HJMC_EINVAL, "N must be >= 1");
+  if (!(c.m0 >= 0.f)) return fail(nullptr, HJMC_EINVAL, "m0 must be >= 0");
+  if (!(c.c_min > 0.f) || !(c.c_min <= c.c_max) || !std::isfinite(c.c_max))
+    return fail(nullptr, HJMC_EINVAL, "need 0 < c_min <= c_max");
+  if (c.visc != HJMC_VISC_PAPER_HALF_LAPLACIAN && c.visc != HJMC_VISC_FULL_LAPLACIAN)
+    return fail(nullptr, HJMC_EINVAL, "visc must be 0 or 1");
+  if (c.crn != 0 && c.crn != 1) return fail(nullptr, HJMC_EINVAL, "crn must be 0 or 1");
+  if (c.antithetic != 0 && c.antithetic != 1) return fail(nullptr, HJMC_EINVAL, "antithetic must be 0 or 1");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return fail(nullptr, HJMC_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (c.device < 0 || c.device >= ndev) return fail(nullptr, HJMC_EINVAL, "device ordinal out of range");
+  hjmc_handle* h = new (std::nothrow) hjmc_handle();
+  if (!h) return fail(nullptr, HJMC_ENOMEM, "host allocation failed");
+  h->cfg = c;
+  if ((e = cudaSetDevice(c.device)) != cudaSuccess ||
+      (e = cudaMalloc((void**)&h->d_err, sizeof(int))) != cudaSuccess ||
+      (e = cudaMalloc((void**)&h->d_bad, sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaMemset(h->d_err, 0, sizeof(int))) != cudaSuccess ||
+      (e = cudaMemset(h->d_bad, 0xFF, sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&h->host_stream, cudaStreamNonBlocking)) != cudaSuccess) {
+    std::string msg = std::string("device setup failed: ") + cudaGetErrorString(e);
+    hjmc_destroy(h);
+    return fail(nullptr, HJMC_ECUDA, msg);
+  }
+  *out = h;
+  return HJMC_OK;
+}
+
+void hjmc_destroy(hjmc_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->cfg.device);
+  cudaDeviceSynchronize();
+  if (h->d_err) cudaFree(h->d_err);
+  if (h->d_bad) cudaFree(h->d_bad);
+  if (h->d_g0) cudaFree(h->d_g0);
+  if (h->d_vfinal) cudaFree(h->d_vfinal);
+  if (h->d_stage) cudaFree(h->d_stage);
+  if (h->host_stream) cudaStreamDestroy(h->host_stream);
+  delete h;
+}
+
+int hjmc_set_dynamics(hjmc_handle* h, int32_t id, const float* params, int32_t np) {
+  if (!h) return HJMC_EINVAL;
+  const int n = h->cfg.n;
+  int want = 0;
+  switch (id) {
+    case HJMC_SYS_QUADRATIC: want = 0; break;
+    case HJMC_SYS_DUBINS_REL:
+      if (n != 3) return fail(h, HJMC_EINVAL, "DUBINS_REL needs n == 3");
+      want = 3;
+      break;
+    case HJMC_SYS_ROCKET6:
+      if (n != 6) return fail(h, HJMC_EINVAL, "ROCKET6 needs n == 6");
+      want = 3;
+      break;
+    case HJMC_SYS_DUBINS_PAIRS:
+      if (n % 3 != 0) return fail(h, HJMC_EINVAL, "DUBINS_PAIRS needs n = 3K");
+      want = 3;
+      break;
+    default: return fail(h, HJMC_EINVAL, "unknown system id");
+  }
+  if (np != 0 && np != want) return fail(h, HJMC_EINVAL, "wrong number of system parameters");
+  if (np > 0 && !params) return fail(h, HJMC_EINVAL, "params is NULL");
+  SystemParams sp{};
+  sp.id = id;
+  sp.n = n;
+  sp.np = np;
+  for (int i = 0; i < np; ++i) {
+    if (!std::isfinite(params[i])) return fail(h, HJMC_EINVAL, "non-finite system parameter");
+    sp.p[i] = params[i];
+  }
+  h->sp = sp;
+  h->sys_set = true;
+  return HJMC_OK;
+}
+
+int hjmc_supported(int32_t target_id, int32_t n) {
+  KernelSet ks;
+  return lookup_kernels(target_id, n, &ks) ? 1 : 0;
+}
+
+int hjmc_set_target(hjmc_handle* h, int32_t id, const float* params, int32_t np) {
+  if (!h) return HJMC_EINVAL;
+  const int n = h->cfg.n;
+  int want_max = 1, want_min = 0;
+  switch (id) {
+    case HJMC_TGT_QUAD_BOWL: break;
+    case HJMC_TGT_DISK:
+      if (n < 2) return fail(h, HJMC_EINVAL, "DISK needs n >= 2");
+      break;
+    case HJMC_TGT_REL_DISK6:
+      if (n != 6) return fail(h, HJMC_EINVAL, "REL_DISK6 needs n == 6");
+      break;
+    case HJMC_TGT_PAIR_UNION:
+      if (n % 3 != 0) return fail(h, HJMC_EINVAL, "PAIR_UNION needs n = 3K");
+      break;
+    case HJMC_TGT_LINEAR:
+      want_min = want_max = n + 1;
+      break;
+    case HJMC_TGT_CONST: break;
+    default: return fail(h, HJMC_EINVAL, "unknown target id");
+  }
+  if (np < want_min || np > want_max) return fail(h, HJMC_EINVAL, "wrong number of target parameters");
+  if (np > 0 && !params) return fail(h, HJMC_EINVAL, "params is NULL");
+  KernelSet ks;
+  if (!lookup_kernels(id, n, &ks))
+    return fail(h, HJMC_EUNSUPPORTED, "no kernel compiled for this (target, n)");
+  TargetParams tp{};
+  tp.np = np;
+  for (int i = 0; i < np; ++i) {
+    if (!std::isfinite(params[i])) return fail(h, HJMC_EINVAL, "non-finite target parameter");
+    tp.p[i] = params[i];
+  }
+  h->tp = tp;
+  h->tgt_id = id;
+  h->ks = ks;
+  h->tgt_set = true;
+  return HJMC_OK;
+}
+
+int hjmc_value_grad(hjmc_handle* h, const float* x, const float* c, const uint32_t* qid,
+                    uint32_t qid_base, int64_t M, float tau, uint32_t j_tag, uint32_t k_tag,
+                    const float* drift, float* v, float* dv, void* stream) {
+  int rc = ready(h);
+  if (rc) return rc;
+  if (M < 0) return fail(h, HJMC_EINVAL, "M < 0");
+  if (M == 0) return HJMC_OK;
+  if (!x || !v) return fail(h, HJMC_EINVAL, "x and v are required");
+  if (!(tau >= 0.f) || !std::isfinite(tau)) return fail(h, HJMC_EINVAL, "tau must be >= 0");
+  if (tau > 0.f && !c) return fail(h, HJMC_EINVAL, "c is required for tau > 0");
+  if (j_tag > 65535u || k_tag > 255u) return fail(h, HJMC_EINVAL, "j_tag <= 65535, k_tag <= 255");
+  if ((rc = set_device(h))) return rc;
+  SolveParams p;
+  fill_common(h, &p);
+  p.x = x;
+  p.drift = drift;
+  p.qid = qid;
+  p.qid_base = qid_base;
+  p.M = M;
+  p.K = 1;
+  p.Kp = 1;
+  p.T = tau;
+  p.mode = kModeValueGrad;
+  p.c_in = c;
+  p.tau_vg = (double)tau;
+  p.jtag = j_tag;
+  p.ktag = k_tag;
+  p.v = v;
+  p.dv = dv;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = h->ks.solve(p, M, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "value_grad launch");
+  return sync_check_if_requested(h, s);
+}
+
+int hjmc_solve_slice(hjmc_handle* h, const float* x, const uint32_t* qid, uint32_t qid_base,
+                     int64_t M, const float* drift, const hjmc_result* out, void* stream) {
+  int rc = ready(h);
+  if (rc) return rc;
+  if (M < 0) return fail(h, HJMC_EINVAL, "M < 0");
+  if (M == 0) return HJMC_OK;
+  if (!x) return fail(h, HJMC_EINVAL, "x is required");
+  if (!out) return fail(h, HJMC_EINVAL, "out is required");
+  const int64_t units = M * (int64_t)h->cfg.K;
+  if (units > 0x7FFFFFFFLL) return fail(h, HJMC_EINVAL, "M*K exceeds the grid limit 2^31-1");
+  if ((rc = set_device(h))) return rc;
+  const bool want_tube = out->tube != nullptr;
+  float* g0 = out->g0;
+  if (want_tube && !g0) {
+    if ((rc = ensure(h, &h->d_g0, &h->g0_cap, (size_t)M))) return rc;
+    g0 = h->d_g0;
+  }
+  float* vfinal = nullptr;
+  if (want_tube) {
+    if ((rc = ensure(h, &h->d_vfinal, &h->vfinal_cap, (size_t)M * (size_t)h->cfg.K))) return rc;
+    vfinal = h->d_vfinal;
+  }
+  SolveParams p;
+  fill_common(h, &p);
+  p.x = x;
+  p.drift = drift;
+  p.qid = qid;
+  p.qid_base = qid_base;
+  p.M = M;
+  p.K = h->cfg.K;
+  p.Kp = h->cfg.Kp;
+  p.T = (double)h->cfg.T;
+  p.mode = kModeSolve;
+  p.v = out->v;
+  p.dv = out->dv;
+  p.c_out = out->c;
+  p.vhist = out->vhist;
+  p.chist = out->chist;
+  p.vfinal = vfinal;
+  p.g0 = g0;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = h->ks.solve(p, units, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "solve launch");
+  if (want_tube) {
+    e = launch_tube(g0, vfinal, h->cfg.K, M, out->tube, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "tube launch");
+  }
+  return sync_check_if_requested(h, s);
+}
+
+int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, uint32_t qid_base, int64_t M,
+                          const float* drift_host, const hjmc_result* out_host) {
+  int rc = ready(h);
+  if (rc) return rc;
+  if (M < 0) return fail(h, HJMC_EINVAL, "M < 0");
+  if (M == 0) return HJMC_OK;
+  if (!x_host || !out_host) return fail(h, HJMC_EINVAL, "x_host and out_host are required");
+  if ((rc = set_device(h))) return rc;
+  const size_t n = (size_t)h->cfg.n, K = (size_t)h->cfg.K, Kp = (size_t)h->cfg.Kp, m = (size_t)M;
+  // staging layout: x | drift | v | dv | c | tube | vhist | chist | g0
+  const size_t sizes[9] = {m * n, drift_host ? m * n : 0, out_host->v ? m : 0,
+                           out_host->dv ? m * n : 0, out_host->c ? m : 0, out_host->tube ? m : 0,
+                           out_host->vhist ? K * Kp * m : 0, out_host->chist ? K * Kp * m : 0,
+                           out_host->g0 ? m : 0};
+  size_t total = 0, off[9];
+  for (int i = 0; i < 9; ++i) {
+    off[i] = total;
+    total += (sizes[i] + 63) & ~size_t(63);  // 256-byte aligned sub-buffers
+  }
+  if ((rc = ensure(h, &h->d_stage, &h->stage_cap, total))) return rc;
+  float* base = h->d_stage;
+  cudaStream_t s = h->host_stream;
+  cudaError_t e = cudaMemcpyAsync(base + off[0], x_host, sizes[0] * sizeof(float),
+                                  cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && drift_host)
+    e = cudaMemcpyAsync(base + off[1], drift_host, sizes[1] * sizeof(float), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "H2D copy");
+  hjmc_result dres{};
+  float** dptr[7] = {&dres.v, &dres.dv, &dres.c, &dres.tube, &dres.vhist, &dres.chist, &dres.g0};
+  for (int i = 0; i < 7; ++i) *dptr[i] = sizes[2 + i] ? base + off[2 + i] : nullptr;
+  rc = hjmc_solve_slice(h, base + off[0], nullptr, qid_base, M, drift_host ? base + off[1] : nullptr,
+                        &dres, (void*)s);
+  if (rc) return rc;
+  float* hptr[7] = {out_host->v, out_host->dv, out_host->c, out_host->tube, out_host->vhist,
+                    out_host->chist, out_host->g0};
+  for (int i = 0; i < 7; ++i) {
+    if (!sizes[2 + i]) continue;
+    e = cudaMemcpyAsync(hptr[i], base + off[2 + i], sizes[2 + i] * sizeof(float),
+                        cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(h, e, "D2H copy");
+  }
+  return hjmc_check(h, (void*)s);
+}
+
+int hjmc_eval_target(hjmc_handle* h, const float* x, int64_t M, float* g, float* dg, void* stream) {
+  if (!h) return HJMC_EINVAL;
+  if (!h->tgt_set) return fail(h, HJMC_EINVAL, "hjmc_set_target has not been called");
+  if (M < 0 || (M > 0 && !x)) return fail(h, HJMC_EINVAL, "bad x / M");
+  if (M == 0) return HJMC_OK;
+  int rc = set_device(h);
+  if (rc) return rc;
+  EvalParams p{};
+  p.x = x;
+  p.M = M;
+  p.g = g;
+  p.dg = dg;
+  p.tp = h->tp;
+  cudaError_t e = h->ks.eval_target(p, (cudaStream_t)stream);
+  return e == cudaSuccess ? HJMC_OK : cuda_fail(h, e, "eval_target launch");
+}
+
+int hjmc_eval_hamiltonian(hjmc_handle* h, const float* x, const float* p_in, int64_t M, float* H,
+                          float* c, void* stream) {
+  if (!h) return HJMC_EINVAL;
+  if (!h->sys_set) return fail(h, HJMC_EINVAL, "hjmc_set_dynamics has not been called");
+  if (M < 0 || (M > 0 && (!x || !p_in))) return fail(h, HJMC_EINVAL, "bad x / p / M");
+  if (M == 0) return HJMC_OK;
+  int rc = set_device(h);
+  if (rc) return rc;
+  EvalParams p{};
+  p.x = x;
+  p.p = p_in;
+  p.M = M;
+  p.H = H;
+  p.c = c;
+  p.sp = h->sp;
+  p.gp.delta_eff = delta_eff(h->cfg);
+  p.gp.m0 = h->cfg.m0;
+  p.gp.c_min = h->cfg.c_min;
+  p.gp.c_max = h->cfg.c_max;
+  cudaError_t e = launch_hamiltonian(p, (cudaStream_t)stream);
+  return e == cudaSuccess ? HJMC_OK : cuda_fail(h, e, "hamiltonian launch");
+}
+
+int hjmc_debug_normals(hjmc_handle* h, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
+                       uint32_t count, float* z, uint32_t* raw, void* stream) {
+  if (!h) return HJMC_EINVAL;
+  if (count > 0 && !z) return fail(h, HJMC_EINVAL, "z is NULL");
+  if (jw > 65535u || kw > 255u) return fail(h, HJMC_EINVAL, "jw <= 65535, kw <= 255");
+  int rc = set_device(h);
+  if (rc) return rc;
+  Key key{(uint32_t)(h->cfg.seed & 0xFFFFFFFFull), (uint32_t)(h->cfg.seed >> 32)};
+  cudaError_t e = launch_debug_normals(h->cfg.n, qid, jw, kw, i0, count, key, h->cfg.tag,
+                                       h->cfg.antithetic, z, raw, (cudaStream_t)stream);
+  return e == cudaSuccess ? HJMC_OK : cuda_fail(h, e, "debug_normals launch");
+}
+
+int hjmc_check(hjmc_handle* h, void* stream) {
+  if (!h) return HJMC_EINVAL;
+  int rc = set_device(h);
+  if (rc) return rc;
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "stream synchronize");
+  int flag = 0;
+  unsigned long long bad = 0;
+  if ((e = cudaMemcpy(&flag, h->d_err, sizeof(int), cudaMemcpyDeviceToHost)) != cudaSuccess ||
+      (e = cudaMemcpy(&bad, h->d_bad, sizeof(bad), cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return cuda_fail(h, e, "error-word read");
+  if (!flag) return HJMC_OK;
+  h->last_bad = (int64_t)bad;
+  cudaMemset(h->d_err, 0, sizeof(int));
+  cudaMemset(h->d_bad, 0xFF, sizeof(unsigned long long));
+  char buf[128];
+  std::snprintf(buf, sizeof(buf), "non-finite v or Dv at global query id %lld", (long long)bad);
+  return fail(h, HJMC_ENUMERIC, buf);
+}
+
+int64_t hjmc_last_bad_query(const hjmc_handle* h) { return h ? h->last_bad : -1; }
+
+const char* hjmc_last_error(const hjmc_handle* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+int hjmc_residual_partials(const float* vhist, const float* g0, int32_t K, int32_t Kp, int64_t M,
+                           double* out) {
+  if (!vhist || !g0 || !out || K < 1 || Kp < 1 || M < 0) return HJMC_EINVAL;
+  for (int j = 0; j < K; ++j) {
+    for (int k = 0; k < Kp; ++k) {
+      double num = 0.0, den = 0.0;
+      const float* cur = vhist + ((size_t)j * Kp + k) * (size_t)M;
+      const float* prev = (k == 0) ? g0 : vhist + ((size_t)j * Kp + (k - 1)) * (size_t)M;
+      for (int64_t m = 0; m < M; ++m) {
+        const double a = (double)cur[m], b = (double)prev[m];
+        num += (a - b) * (a - b);
+        den += b * b;
+      }
+      out[((size_t)j * Kp + k) * 2 + 0] = num;
+      out[((size_t)j * Kp + k) * 2 + 1] = den;
+    }
+  }
+  return HJMC_OK;
+}
+
+}  // extern "C"

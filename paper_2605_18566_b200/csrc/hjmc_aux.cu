@@ -1,0 +1,81 @@
+// hjmc_aux.cu — small non-templated kernels: tube epilogue, H/Γ evaluator, RNG debug dump.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hjmc_kernels.cuh"
+
+namespace hjmc {
+
+namespace {
+
+__global__ void tube_kernel(const float* __restrict__ g0, const float* __restrict__ vfinal, int K,
+                            int64_t M, float* __restrict__ tube) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  float t = g0[m];  // running min including g
+  for (int j = 0; j < K; ++j) t = fminf(t, vfinal[(size_t)j * (size_t)M + (size_t)m]);
+  tube[m] = t;
+}
+
+__global__ void hamiltonian_kernel(const EvalParams P) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= P.M) return;
+  const int n = P.sp.n;
+  double x[64], p[64];
+  for (int d = 0; d < n; ++d) {
+    x[d] = (double)P.x[m * n + d];
+    p[d] = (double)P.p[m * n + d];
+  }
+  if (P.H) P.H[m] = (float)hamiltonian(P.sp, x, p);
+  if (P.c) P.c[m] = (float)gamma_update(P.sp, P.gp, x, p);
+}
+
+__global__ void debug_normals_kernel(int n, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
+                                     uint32_t count, Key key, uint32_t tag, int antithetic,
+                                     float* z, uint32_t* raw) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= count) return;
+  const uint32_t i = i0 + s;
+  const uint32_t draw = antithetic ? (i >> 1) : i;
+  const float sign = (antithetic && (i & 1u)) ? -1.f : 1.f;
+  const int quads = (n + 3) / 4;
+  for (int b = 0; b < quads; ++b) {
+    const uint4 w = philox4x32_10(draw, ctr_word1((uint32_t)b, kw, jw), qid, tag, key);
+    if (raw) {
+      uint32_t* r = raw + (size_t)s * 4 * quads + 4 * b;
+      r[0] = w.x; r[1] = w.y; r[2] = w.z; r[3] = w.w;
+    }
+    float t[4];
+    box_muller<true>(w.x, w.y, t[0], t[1]);
+    box_muller<true>(w.z, w.w, t[2], t[3]);
+    for (int e = 0; e < 4; ++e)
+      if (4 * b + e < n) z[(size_t)s * n + 4 * b + e] = sign * t[e];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_tube(const float* g0, const float* vfinal, int K, int64_t M, float* tube,
+                        cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  tube_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(g0, vfinal, K, M, tube);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hamiltonian(const EvalParams& p, cudaStream_t s) {
+  if (p.M <= 0) return cudaSuccess;
+  hamiltonian_kernel<<<(unsigned)((p.M + 127) / 128), 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_debug_normals(int n, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
+                                 uint32_t count, Key key, uint32_t tag, int antithetic, float* z,
+                                 uint32_t* raw, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  debug_normals_kernel<<<(count + 127) / 128, 128, 0, s>>>(n, qid, jw, kw, i0, count, key, tag,
+                                                           antithetic, z, raw);
+  return cudaGetLastError();
+}
+
+}  // namespace hjmc

@@ -1,0 +1,13 @@
+// hjmc_dispatch.cu — (target id, n) → compiled kernel set (ids as in include/hjmc.h).
+#include "hjmc_kernels.cuh"
+
+namespace hjmc {
+bool lookup_basic(int target, int n, KernelSet* out);
+bool lookup_games(int target, int n, KernelSet* out);
+bool lookup_highdim(int target, int n, KernelSet* out);
+
+bool lookup_kernels(int target, int n, KernelSet* out) {
+  return lookup_basic(target, n, out) || lookup_games(target, n, out) ||
+         lookup_highdim(target, n, out);
+}
+}  // namespace hjmc

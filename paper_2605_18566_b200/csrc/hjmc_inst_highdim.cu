@@ -1,0 +1,15 @@
+// hjmc_inst_highdim.cu — kernel instantiations: K-pair union (configs 4–5) and high-n bowls.
+#include "hjmc_solve_impl.cuh"
+
+namespace hjmc {
+bool lookup_highdim(int target, int n, KernelSet* out) {
+  HJMC_CASE(3, PairUnion, 3)
+  HJMC_CASE(3, PairUnion, 6)
+  HJMC_CASE(3, PairUnion, 9)
+  HJMC_CASE(3, PairUnion, 15)
+  HJMC_CASE(3, PairUnion, 45)
+  HJMC_CASE(0, QuadBowl, 15)
+  HJMC_CASE(0, QuadBowl, 45)
+  return false;
+}
+}  // namespace hjmc

@@ -1,0 +1,331 @@
+// hjmc_solve_impl.cuh — the fused Monte-Carlo Picard kernel (SURVEY §8(a) rows a1–a11).
+//
+// One CTA owns one work unit = (query m, horizon j) and runs the whole Picard loop of that
+// horizon (Algorithm 1) without leaving the SM: queries and horizons are mutually
+// independent (R5, R9), so no grid-wide synchronisation or inter-CTA traffic exists.
+// Per Picard iterate (one Φ pass):
+//   every thread walks a strided subset of the N samples; per sample it regenerates its
+//   normals from Philox in registers (no sample array in memory), forms y = x + σz, evaluates
+//   g, and accumulates w = 2^(A·core + B) and w·z (A = −c log2 e; B a guaranteed-safe shift,
+//   hjmc_targets.cuh) — one FFMA + one MUFU.EX2 per weight, no per-sample max or rescale;
+//   then a warp-shuffle butterfly and a shared-memory merge across warps give the CTA sums,
+//   and thread 0 forms v, Dv and the next frozen coefficient c = Γ(x, Dv) in double.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hjmc_kernels.cuh"
+
+namespace hjmc {
+
+namespace {
+
+constexpr double kLog2e = 1.4426950408889634074;
+constexpr double kLn2 = 0.69314718055994530942;
+constexpr float kUnderflowS = 7.888609052210118e-31f;  // 2^-100: fallback threshold
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Accumulate the weighted sums of one Φ pass over this thread's samples.
+//   S += w,  Mz[d] += w z_d,  w = 2^(A core(y) + B)
+template <class Tgt, int NDIM, int NT>
+__device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[NDIM], float sigma,
+                                              float A, float B, uint32_t N, int antithetic,
+                                              uint32_t w1base, uint32_t qid, uint32_t tag, Key key,
+                                              float& S, float (&Mz)[NDIM]) {
+  S = 0.f;
+#pragma unroll
+  for (int d = 0; d < NDIM; ++d) Mz[d] = 0.f;
+  if (!antithetic) {
+#pragma unroll 2
+    for (uint32_t i = threadIdx.x; i < N; i += NT) {
+      float z[NDIM];
+      sample_normals<NDIM>(z, i, w1base, qid, tag, key);
+      const float w = ex2_approx(fmaf(A, tgt.core(xs, sigma, z), B));
+      S += w;
+#pragma unroll
+      for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(w, z[d], Mz[d]);
+    }
+  } else {
+    const uint32_t draws = (N >> 1) + (N & 1u);
+    for (uint32_t q = threadIdx.x; q < draws; q += NT) {
+      float z[NDIM];
+      sample_normals<NDIM>(z, q, w1base, qid, tag, key);
+      const float wp = ex2_approx(fmaf(A, tgt.core(xs, sigma, z), B));
+      const float wm = (2 * q + 1 < N) ? ex2_approx(fmaf(A, tgt.core(xs, -sigma, z), B)) : 0.f;
+      S += wp + wm;
+      const float dw = wp - wm;
+#pragma unroll
+      for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(dw, z[d], Mz[d]);
+    }
+  }
+}
+
+// Largest exponent A·core(y_i) over this thread's samples (fallback shift; rarely used).
+template <class Tgt, int NDIM, int NT>
+__device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float sigma, float A,
+                                 uint32_t N, int antithetic, uint32_t w1base, uint32_t qid,
+                                 uint32_t tag, Key key) {
+  float amax = -3.0e38f;
+  if (!antithetic) {
+    for (uint32_t i = threadIdx.x; i < N; i += NT) {
+      float z[NDIM];
+      sample_normals<NDIM>(z, i, w1base, qid, tag, key);
+      amax = fmaxf(amax, A * tgt.core(xs, sigma, z));
+    }
+  } else {
+    const uint32_t draws = (N >> 1) + (N & 1u);
+    for (uint32_t q = threadIdx.x; q < draws; q += NT) {
+      float z[NDIM];
+      sample_normals<NDIM>(z, q, w1base, qid, tag, key);
+      amax = fmaxf(amax, A * tgt.core(xs, sigma, z));
+      if (2 * q + 1 < N) amax = fmaxf(amax, A * tgt.core(xs, -sigma, z));
+    }
+  }
+  return amax;
+}
+
+template <int NDIM, int NT>
+struct SolveSmem {
+  float part[NT / 32][NDIM + 1];
+  double sum[NDIM + 1];
+  float fmax_part[NT / 32];
+  double c_next;
+  float shift;
+};
+
+// CTA-wide merge of (S, Mz[NDIM]) into sm.sum (double), deterministic order.
+template <int NDIM, int NT>
+__device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, float (&Mz)[NDIM]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  S = warp_sum(S);
+#pragma unroll
+  for (int d = 0; d < NDIM; ++d) Mz[d] = warp_sum(Mz[d]);
+  if (lane == 0) {
+    sm.part[warp][0] = S;
+#pragma unroll
+    for (int d = 0; d < NDIM; ++d) sm.part[warp][1 + d] = Mz[d];
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < NDIM + 1; col += NT) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) acc += (double)sm.part[w][col];
+    sm.sum[col] = acc;
+  }
+  __syncthreads();
+}
+
+// Thread 0's per-iterate epilogue (a9–a10), double precision: v and Dv from the CTA sums,
+// outputs, and the next frozen coefficient Γ(x, Dv) (returned; solve mode only).
+template <class Tgt, int NDIM>
+__device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tgt, int64_t m, int j,
+                                             int k, uint32_t id, double c, double sigma_d,
+                                             float A, float B, float core_ref, const double* sum) {
+  const double A_d = -c * kLog2e;
+  const double Ssum = sum[0];
+  // log2 of (1/N) Σ exp(−c g_i): undo the shift B and the fp32 rounding of A
+  const double log2mean = log2(Ssum) - log2((double)P.N) - (double)B + A_d * (double)tgt.off +
+                          (A_d - (double)A) * (double)core_ref;
+  const double v = -(kLn2 / c) * log2mean;                           // Cor. logsumexp
+  double dv[NDIM];
+  bool finite = isfinite(v);
+  for (int d = 0; d < NDIM; ++d) {
+    dv[d] = -(sum[1 + d] / Ssum) / (c * sigma_d);                     // Cor. mc_gradient
+    finite = finite && isfinite(dv[d]);
+  }
+  if (!finite && P.err) {
+    atomicOr(P.err, 1);
+    atomicMin(P.bad, (unsigned long long)id);
+  }
+  const bool last = (k == P.Kp - 1);
+  if (P.mode != kModeSolve) {
+    if (P.v) P.v[m] = (float)v;
+    if (P.dv)
+      for (int d = 0; d < NDIM; ++d) P.dv[m * NDIM + d] = (float)dv[d];
+    return c;
+  }
+  const size_t hi = ((size_t)(j - 1) * (size_t)P.Kp + (size_t)k) * (size_t)P.M + (size_t)m;
+  if (P.vhist) P.vhist[hi] = (float)v;
+  if (P.chist) P.chist[hi] = (float)c;
+  double xd[NDIM];
+  for (int d = 0; d < NDIM; ++d) xd[d] = (double)P.x[m * NDIM + d];
+  const double c_next = gamma_update(P.sp, P.gp, xd, dv);           // Γ; dv → p̃
+  if (last) {
+    if (P.vfinal) P.vfinal[(size_t)(j - 1) * (size_t)P.M + (size_t)m] = (float)v;
+    if (j == P.K) {
+      if (P.v) P.v[m] = (float)v;
+      if (P.dv)
+        for (int d = 0; d < NDIM; ++d)
+          P.dv[m * NDIM + d] = (float)(-(sum[1 + d] / Ssum) / (c * sigma_d));
+      if (P.c_out) P.c_out[m] = (float)c_next;
+    }
+  }
+  return c_next;
+}
+
+// Thread 0's prologue: g(x) output, τ = 0 point-mass case, and c^(0) = Γ(x, Dg(x))
+// (Algorithm 1 init) or the caller's frozen c (value_grad). Returns c (0 when
+// the unit is complete because σ = 0; the caller flags that case).
+template <class Tgt, int NDIM>
+__device__ __noinline__ double unit_prologue(const SolveParams& P, const Tgt& tgt, int64_t m, int j,
+                                             double sigma_d, const float* xs) {
+  double xd[NDIM], p[NDIM];
+  for (int d = 0; d < NDIM; ++d) xd[d] = (double)P.x[m * NDIM + d];
+  if (P.mode == kModeSolve && j == 1 && P.g0) P.g0[m] = (float)tgt.g_host(xd);
+  if (sigma_d == 0.0) {  // τ = 0: point mass, v = g(x), Dv = Dg(x)
+    for (int d = 0; d < NDIM; ++d) xd[d] = (double)xs[d];
+    if (P.v) P.v[m] = (float)tgt.g_host(xd);
+    tgt.dg(xd, p);
+    if (P.dv)
+      for (int d = 0; d < NDIM; ++d) P.dv[m * NDIM + d] = (float)p[d];
+    return 0.0;
+  }
+  if (P.mode != kModeSolve) return (double)P.c_in[m];
+  tgt.dg(xd, p);
+  return gamma_update(P.sp, P.gp, xd, p);
+}
+
+template <class Tgt, int NDIM, int NT>
+__global__ void __launch_bounds__(NT) solve_kernel(const __grid_constant__ SolveParams P) {
+  __shared__ SolveSmem<NDIM, NT> sm;
+  const int64_t unit = blockIdx.x;
+  int64_t m;
+  int j;
+  if (P.mode == kModeSolve) {
+    m = unit / P.K;
+    j = (int)(unit % P.K) + 1;
+  } else {
+    m = unit;
+    j = 1;
+  }
+  const Tgt tgt(P.tp);
+
+  // a1: query staging (uniform across the CTA; served from L1 after the first warp)
+  const uint32_t id = P.qid ? P.qid[m] : P.qid_base + (uint32_t)m;
+  const double tau = (P.mode == kModeSolve) ? (double)j * P.T / (double)P.K : P.tau_vg;
+  const double sigma_d = sqrt(P.gp.delta_eff * tau);
+  const float sigma = (float)sigma_d;
+  float xs[NDIM];
+#pragma unroll
+  for (int d = 0; d < NDIM; ++d) {
+    const float xv = P.x[m * NDIM + d];
+    xs[d] = P.drift ? __fadd_rn(xv, __fmul_rn(P.drift[m * NDIM + d], (float)tau)) : xv;
+  }
+
+  if (threadIdx.x == 0) {
+    sm.c_next = unit_prologue<Tgt, NDIM>(P, tgt, m, j, sigma_d, xs);
+    sm.shift = (sigma_d == 0.0) ? 1.f : 0.f;
+  }
+  __syncthreads();
+  double c = sm.c_next;
+  if (sm.shift != 0.f) return;  // σ = 0: handled by the prologue (uniform branch)
+  __syncthreads();
+
+  const uint32_t jw = (P.mode == kModeSolve) ? (uint32_t)j : P.jtag;
+  float core_ref;
+  {
+    float z0[NDIM];
+#pragma unroll
+    for (int d = 0; d < NDIM; ++d) z0[d] = 0.f;
+    core_ref = tgt.core(xs, 0.f, z0);
+  }
+  const float lowc = tgt.core_lower(xs, sigma);
+
+  for (int k = 0; k < P.Kp; ++k) {
+    const uint32_t kw = (P.mode == kModeSolve) ? (P.crn ? 0u : (uint32_t)k) : P.ktag;
+    const uint32_t w1base = (kw << 8) | (jw << 16);
+    const float A = (float)(-c * kLog2e);
+    float B = -A * lowc;  // every a_i = A core_i + B ≤ 0: no weight can overflow
+
+    float S, Mz[NDIM];
+    mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma, A, B, P.N, P.antithetic, w1base, id, P.tag,
+                                 P.key, S, Mz);
+    cta_reduce<NDIM, NT>(sm, S, Mz);
+    if (!(sm.sum[0] >= (double)kUnderflowS)) {
+      // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with
+      // the exact maximum exponent, the plain two-pass log-sum-exp.
+      const float amax = warp_max(mc_max_exponent<Tgt, NDIM, NT>(
+          tgt, xs, sigma, A, P.N, P.antithetic, w1base, id, P.tag, P.key));
+      if ((threadIdx.x & 31) == 0) sm.fmax_part[threadIdx.x >> 5] = amax;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float mx = sm.fmax_part[0];
+        for (int w = 1; w < NT / 32; ++w) mx = fmaxf(mx, sm.fmax_part[w]);
+        sm.shift = mx;
+      }
+      __syncthreads();
+      B = -sm.shift;
+      mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma, A, B, P.N, P.antithetic, w1base, id, P.tag,
+                                   P.key, S, Mz);
+      cta_reduce<NDIM, NT>(sm, S, Mz);
+    }
+    if (threadIdx.x == 0)
+      sm.c_next = pass_epilogue<Tgt, NDIM>(P, tgt, m, j, k, id, c, sigma_d, A, B, core_ref, sm.sum);
+    __syncthreads();
+    c = sm.c_next;
+    __syncthreads();
+  }
+}
+
+template <class Tgt, int NDIM, int NT>
+cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
+  if (units <= 0) return cudaSuccess;
+  if (units > 0x7FFFFFFFLL) return cudaErrorInvalidValue;
+  solve_kernel<Tgt, NDIM, NT><<<(unsigned)units, NT, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// ---- small kernels ---------------------------------------------------------------------------
+template <class Tgt, int NDIM>
+__global__ void eval_target_kernel(const EvalParams P) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= P.M) return;
+  const Tgt tgt(P.tp);
+  double x[NDIM], dg[NDIM];
+  for (int d = 0; d < NDIM; ++d) x[d] = (double)P.x[m * NDIM + d];
+  if (P.g) P.g[m] = (float)tgt.g_host(x);
+  if (P.dg) {
+    tgt.dg(x, dg);
+    for (int d = 0; d < NDIM; ++d) P.dg[m * NDIM + d] = (float)dg[d];
+  }
+}
+
+template <class Tgt, int NDIM>
+cudaError_t launch_eval_target(const EvalParams& p, cudaStream_t s) {
+  if (p.M <= 0) return cudaSuccess;
+  const int bs = 128;
+  eval_target_kernel<Tgt, NDIM><<<(unsigned)((p.M + bs - 1) / bs), bs, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// One instantiation set per (target, n): the fused solve kernel and the g/Dg evaluator.
+template <template <int> class T, int NDIM>
+KernelSet make_set() {
+  constexpr int kThreads = 256;
+  KernelSet k;
+  k.solve = &launch_solve<T<NDIM>, NDIM, kThreads>;
+  k.eval_target = &launch_eval_target<T<NDIM>, NDIM>;
+  k.threads = kThreads;
+  return k;
+}
+
+}  // namespace
+
+#define HJMC_CASE(TGT_ID, TMPL, NN) \
+  if (target == TGT_ID && n == NN) { \
+    *out = make_set<TMPL, NN>();     \
+    return true;                     \
+  }
+
+}  // namespace hjmc
