@@ -50,7 +50,7 @@
  *    c1 = b | (kw << 8) | (jw << 16)
  *         solve_slice: jw = j (1..K), kw = crn ? 0 : k (0..Kp−1);  value_grad: caller's tags
  *    c2 = global query id;   c3 = config tag
- *  Uniforms from a 32-bit word w:  m = w & 0x7FFFFF;
+ *  Uniforms from a 32-bit word w:  m = w >> 9 (its high 23 bits);
  *    u(w) = (2m + 1) · 2^−24  ∈ (0, 1)       (radius argument, never 0 or 1)
  *    a(w) = m · 2^−23          ∈ [0, 1)       (angle fraction)
  *  Box–Muller, per Philox output (x0, x1, x2, x3) of quad b:

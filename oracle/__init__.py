@@ -65,7 +65,7 @@ def lib():
                               C.c_uint32, dp, dp, dp, dp]
         L.orc_phi.restype = C.c_int
         L.orc_solve_slice.argtypes = [pp, fp, fp, up, C.c_uint32, C.c_int64, dp, dp, dp, dp, dp,
-                                      dp, dp, C.c_int32]
+                                      dp, dp, dp, C.c_int32]
         L.orc_solve_slice.restype = C.c_int
         L.orc_residual_partials.argtypes = [dp, dp, C.c_int32, C.c_int32, C.c_int64, dp]
         L.orc_max_threads.restype = C.c_int
@@ -213,6 +213,7 @@ def solve_slice(P: Problem, x, drift=None, qid_base: int = 0, qids=None, nthread
     out = {
         "v": np.zeros(M), "dv": np.zeros((M, n)), "c": np.zeros(M), "tube": np.zeros(M),
         "vhist": np.zeros((K, Kp, M)), "chist": np.zeros((K, Kp, M)), "g0": np.zeros(M),
+        "dvhist": np.zeros((K, Kp, M, n)),
     }
     b = None if drift is None else np.ascontiguousarray(drift, dtype=np.float32)
     q = None if qids is None else np.ascontiguousarray(qids, dtype=np.uint32)
@@ -221,9 +222,23 @@ def solve_slice(P: Problem, x, drift=None, qid_base: int = 0, qids=None, nthread
         b.ctypes.data_as(C.POINTER(C.c_float)) if b is not None else None,
         q.ctypes.data_as(C.POINTER(C.c_uint32)) if q is not None else None,
         qid_base, M, _dp(out["v"]), _dp(out["dv"]), _dp(out["c"]), _dp(out["tube"]),
-        _dp(out["vhist"]), _dp(out["chist"]), _dp(out["g0"]), nthreads)
+        _dp(out["vhist"]), _dp(out["chist"]), _dp(out["g0"]), _dp(out["dvhist"]), nthreads)
     out["status"] = st
     return out
+
+
+def gamma_sensitivity(P: Problem, x, p, rel: float = 1e-6) -> float:
+    """‖∇_p Γ(x, p)‖₂ by central differences (steps rel·max(|p|, m0)); used by the parity tests
+    to bound how far c = Γ(x, Dv) may move when Dv carries a small relative error."""
+    x = np.asarray(x, dtype=np.float64)
+    p = np.asarray(p, dtype=np.float64)
+    h = rel * max(np.linalg.norm(p), P.m0)
+    g = np.zeros(P.n)
+    for d in range(P.n):
+        e = np.zeros(P.n)
+        e[d] = h
+        g[d] = (gamma(P, x, p + e) - gamma(P, x, p - e)) / (2 * h)
+    return float(np.linalg.norm(g))
 
 
 def residual_partials(vhist, g0):

@@ -43,9 +43,9 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
   out[0] = x0; out[1] = x1; out[2] = x2; out[3] = x3;
 }
 
-/* u(w) = (2m+1)/2^24 in (0,1) and a(w) = m/2^23 in [0,1), m = low 23 bits (R19). */
-static double unif_open(uint32_t w) { return (2.0 * (double)(w & 0x7FFFFFu) + 1.0) / 16777216.0; }
-static double unif_angle(uint32_t w) { return (double)(w & 0x7FFFFFu) / 8388608.0; }
+/* u(w) = (2m+1)/2^24 in (0,1) and a(w) = m/2^23 in [0,1), m = high 23 bits of w (R19). */
+static double unif_open(uint32_t w) { return (2.0 * (double)(w >> 9) + 1.0) / 16777216.0; }
+static double unif_angle(uint32_t w) { return (double)(w >> 9) / 8388608.0; }
 
 /* The n standard normals z_{i,0..n-1} of sample i ("y_i ~ N(0, I_n)"), Box–Muller on
  * Philox words with counter (i, b | kw<<8 | jw<<16, qid, tag), b = quad index (R19). */
@@ -311,12 +311,13 @@ int orc_phi(const orc_problem* P, const double* x, const double* drift, uint32_t
  *   tau_j = j T / K (R9); v^(0) = g; c^(0) = Gamma(x, Dg);
  *   for k: freeze c^(k); (v^(k+1), Dv^(k+1)) = Phi(c^(k)); c^(k+1) = Gamma(x, Dv^(k+1)).
  * Outputs (each may be NULL): v, dv, c at tau_K after the last iterate (c = Gamma of the last
- * Dv); tube = min(g(x), min_j v_j); vhist/chist [K][Kp][M]; g0 [M].
+ * Dv); tube = min(g(x), min_j v_j); vhist/chist [K][Kp][M]; g0 [M]; dvhist [K][Kp][M][n] (the
+ * Dv of every iterate, a diagnostic output for the tests).
  * Queries x arrive as the same fp32 array the GPU receives, converted to double (R22).
  * ---------------------------------------------------------------------------------------- */
 int orc_solve_slice(const orc_problem* P, const float* x, const float* drift, const uint32_t* qid,
                     uint32_t qid_base, int64_t M, double* v, double* dv, double* c, double* tube,
-                    double* vhist, double* chist, double* g0, int32_t nthreads) {
+                    double* vhist, double* chist, double* g0, double* dvhist, int32_t nthreads) {
   int n = P->n, K = P->K, Kp = P->Kp;
   double* vfinal = (double*)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1) * (size_t)(M > 0 ? M : 1));
   if (!vfinal) return 1;
@@ -351,6 +352,7 @@ int orc_solve_slice(const orc_problem* P, const float* x, const float* drift, co
       size_t hi = ((size_t)(j - 1) * (size_t)Kp + (size_t)k) * (size_t)M + (size_t)m;
       if (vhist) vhist[hi] = vk;
       if (chist) chist[hi] = ck;
+      if (dvhist) for (int d = 0; d < n; ++d) dvhist[hi * (size_t)n + d] = dvm[d];
       ck = orc_gamma(P, xm, dvm);
     }
     vfinal[(size_t)(j - 1) * (size_t)M + (size_t)m] = vk;

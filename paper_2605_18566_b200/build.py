@@ -46,15 +46,18 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, extra: list | None = None) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, extra: list | None = None,
+          out: str | None = None, obj_dir: str | None = None) -> str:
+    lib = out or LIB
+    odir = obj_dir or OBJ
+    if not force and out is None and up_to_date():
         return LIB
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(odir, exist_ok=True)
     cc = nvcc()
     extra = list(extra or [])
 
     def compile_one(src):
-        obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+        obj = os.path.join(odir, os.path.basename(src).replace(".cu", ".o"))
         cmd = [cc, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
@@ -66,13 +69,13 @@ def build(force: bool = False, verbose: bool = False, extra: list | None = None)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
         objs = list(ex.map(compile_one, srcs))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [cc, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -74,8 +74,7 @@ double delta_eff(const hjmc_config& c) {
 void fill_common(const hjmc_handle* h, SolveParams* p) {
   std::memset(p, 0, sizeof(*p));
   p->N = h->cfg.N;
-  p->key.k0 = (uint32_t)(h->cfg.seed & 0xFFFFFFFFull);
-  p->key.k1 = (uint32_t)(h->cfg.seed >> 32);
+  make_round_keys(h->cfg.seed, &p->rk);
   p->tag = h->cfg.tag;
   p->crn = h->cfg.crn;
   p->antithetic = h->cfg.antithetic;
@@ -436,8 +435,9 @@ int hjmc_debug_normals(hjmc_handle* h, uint32_t qid, uint32_t jw, uint32_t kw, u
   if (jw > 65535u || kw > 255u) return fail(h, HJMC_EINVAL, "jw <= 65535, kw <= 255");
   int rc = set_device(h);
   if (rc) return rc;
-  Key key{(uint32_t)(h->cfg.seed & 0xFFFFFFFFull), (uint32_t)(h->cfg.seed >> 32)};
-  cudaError_t e = launch_debug_normals(h->cfg.n, qid, jw, kw, i0, count, key, h->cfg.tag,
+  RoundKeys rk;
+  make_round_keys(h->cfg.seed, &rk);
+  cudaError_t e = launch_debug_normals(h->cfg.n, qid, jw, kw, i0, count, rk, h->cfg.tag,
                                        h->cfg.antithetic, z, raw, (cudaStream_t)stream);
   return e == cudaSuccess ? HJMC_OK : cuda_fail(h, e, "debug_normals launch");
 }

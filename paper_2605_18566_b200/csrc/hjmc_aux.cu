@@ -32,8 +32,8 @@ __global__ void hamiltonian_kernel(const EvalParams P) {
 }
 
 __global__ void debug_normals_kernel(int n, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
-                                     uint32_t count, Key key, uint32_t tag, int antithetic,
-                                     float* z, uint32_t* raw) {
+                                     uint32_t count, const __grid_constant__ RoundKeys rk,
+                                     uint32_t tag, int antithetic, float* z, uint32_t* raw) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= count) return;
   const uint32_t i = i0 + s;
@@ -41,16 +41,16 @@ __global__ void debug_normals_kernel(int n, uint32_t qid, uint32_t jw, uint32_t 
   const float sign = (antithetic && (i & 1u)) ? -1.f : 1.f;
   const int quads = (n + 3) / 4;
   for (int b = 0; b < quads; ++b) {
-    const uint4 w = philox4x32_10(draw, ctr_word1((uint32_t)b, kw, jw), qid, tag, key);
+    const uint4 w = philox4x32_10(draw, ctr_word1((uint32_t)b, kw, jw), qid, tag, rk);
     if (raw) {
       uint32_t* r = raw + (size_t)s * 4 * quads + 4 * b;
       r[0] = w.x; r[1] = w.y; r[2] = w.z; r[3] = w.w;
     }
     float t[4];
-    box_muller<true>(w.x, w.y, t[0], t[1]);
-    box_muller<true>(w.z, w.w, t[2], t[3]);
+    box_muller_hat<true>(w.x, w.y, t[0], t[1]);
+    box_muller_hat<true>(w.z, w.w, t[2], t[3]);
     for (int e = 0; e < 4; ++e)
-      if (4 * b + e < n) z[(size_t)s * n + 4 * b + e] = sign * t[e];
+      if (4 * b + e < n) z[(size_t)s * n + 4 * b + e] = sign * kBMScale * t[e];
   }
 }
 
@@ -70,10 +70,10 @@ cudaError_t launch_hamiltonian(const EvalParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_debug_normals(int n, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
-                                 uint32_t count, Key key, uint32_t tag, int antithetic, float* z,
-                                 uint32_t* raw, cudaStream_t s) {
+                                 uint32_t count, const RoundKeys& rk, uint32_t tag, int antithetic,
+                                 float* z, uint32_t* raw, cudaStream_t s) {
   if (count == 0) return cudaSuccess;
-  debug_normals_kernel<<<(count + 127) / 128, 128, 0, s>>>(n, qid, jw, kw, i0, count, key, tag,
+  debug_normals_kernel<<<(count + 127) / 128, 128, 0, s>>>(n, qid, jw, kw, i0, count, rk, tag,
                                                            antithetic, z, raw);
   return cudaGetLastError();
 }

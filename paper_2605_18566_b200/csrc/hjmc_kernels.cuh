@@ -23,7 +23,7 @@ struct SolveParams {
   double tau_vg;           // value_grad: τ
   uint32_t jtag, ktag;     // value_grad: counter tags
   uint32_t N;
-  Key key;
+  RoundKeys rk;            // Philox round keys of cfg.seed
   uint32_t tag;
   int crn, antithetic;
   GammaParams gp;
@@ -72,7 +72,7 @@ cudaError_t launch_tube(const float* g0, const float* vfinal, int K, int64_t M, 
                         cudaStream_t s);
 cudaError_t launch_hamiltonian(const EvalParams& p, cudaStream_t s);
 cudaError_t launch_debug_normals(int n, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
-                                 uint32_t count, Key key, uint32_t tag, int antithetic, float* z,
+                                 uint32_t count, const RoundKeys& rk, uint32_t tag, int antithetic, float* z,
                                  uint32_t* raw, cudaStream_t s);
 
 }  // namespace hjmc

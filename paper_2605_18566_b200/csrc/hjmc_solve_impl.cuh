@@ -41,7 +41,7 @@ __device__ __forceinline__ float warp_max(float v) {
 template <class Tgt, int NDIM, int NT>
 __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[NDIM], float sigma,
                                               float A, float B, uint32_t N, int antithetic,
-                                              uint32_t w1base, uint32_t qid, uint32_t tag, Key key,
+                                              uint32_t w1base, uint32_t qid, uint32_t tag, const RoundKeys& rk,
                                               float& S, float (&Mz)[NDIM]) {
   S = 0.f;
 #pragma unroll
@@ -50,7 +50,7 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
 #pragma unroll 2
     for (uint32_t i = threadIdx.x; i < N; i += NT) {
       float z[NDIM];
-      sample_normals<NDIM>(z, i, w1base, qid, tag, key);
+      sample_normals_hat<NDIM>(z, i, w1base, qid, tag, rk);
       const float w = ex2_approx(fmaf(A, tgt.core(xs, sigma, z), B));
       S += w;
 #pragma unroll
@@ -60,7 +60,7 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
     const uint32_t draws = (N >> 1) + (N & 1u);
     for (uint32_t q = threadIdx.x; q < draws; q += NT) {
       float z[NDIM];
-      sample_normals<NDIM>(z, q, w1base, qid, tag, key);
+      sample_normals_hat<NDIM>(z, q, w1base, qid, tag, rk);
       const float wp = ex2_approx(fmaf(A, tgt.core(xs, sigma, z), B));
       const float wm = (2 * q + 1 < N) ? ex2_approx(fmaf(A, tgt.core(xs, -sigma, z), B)) : 0.f;
       S += wp + wm;
@@ -75,19 +75,19 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
 template <class Tgt, int NDIM, int NT>
 __device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float sigma, float A,
                                  uint32_t N, int antithetic, uint32_t w1base, uint32_t qid,
-                                 uint32_t tag, Key key) {
+                                 uint32_t tag, const RoundKeys& rk) {
   float amax = -3.0e38f;
   if (!antithetic) {
     for (uint32_t i = threadIdx.x; i < N; i += NT) {
       float z[NDIM];
-      sample_normals<NDIM>(z, i, w1base, qid, tag, key);
+      sample_normals_hat<NDIM>(z, i, w1base, qid, tag, rk);
       amax = fmaxf(amax, A * tgt.core(xs, sigma, z));
     }
   } else {
     const uint32_t draws = (N >> 1) + (N & 1u);
     for (uint32_t q = threadIdx.x; q < draws; q += NT) {
       float z[NDIM];
-      sample_normals<NDIM>(z, q, w1base, qid, tag, key);
+      sample_normals_hat<NDIM>(z, q, w1base, qid, tag, rk);
       amax = fmaxf(amax, A * tgt.core(xs, sigma, z));
       if (2 * q + 1 < N) amax = fmaxf(amax, A * tgt.core(xs, -sigma, z));
     }
@@ -141,7 +141,8 @@ __device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tg
   double dv[NDIM];
   bool finite = isfinite(v);
   for (int d = 0; d < NDIM; ++d) {
-    dv[d] = -(sum[1 + d] / Ssum) / (c * sigma_d);                     // Cor. mc_gradient
+    // Cor. mc_gradient; the sums hold ẑ = z/C (hjmc_rng.cuh), so E_w[z] = C·M̂/S
+    dv[d] = -((double)kBMScale * sum[1 + d] / Ssum) / (c * sigma_d);
     finite = finite && isfinite(dv[d]);
   }
   if (!finite && P.err) {
@@ -167,7 +168,7 @@ __device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tg
       if (P.v) P.v[m] = (float)v;
       if (P.dv)
         for (int d = 0; d < NDIM; ++d)
-          P.dv[m * NDIM + d] = (float)(-(sum[1 + d] / Ssum) / (c * sigma_d));
+          P.dv[m * NDIM + d] = (float)(-((double)kBMScale * sum[1 + d] / Ssum) / (c * sigma_d));
       if (P.c_out) P.c_out[m] = (float)c_next;
     }
   }
@@ -196,8 +197,22 @@ __device__ __noinline__ double unit_prologue(const SolveParams& P, const Tgt& tg
   return gamma_update(P.sp, P.gp, xd, p);
 }
 
+#ifndef HJMC_NT
+#define HJMC_NT 256
+#endif
+// Resident CTAs per SM requested from ptxas (caps registers: 4 → 64 regs at 256 threads).
+// Measured on B200 for C2 (n = 3): 4/SM beats 3/SM by 2% and 1/SM by 7% (profiles/). Larger n
+// needs the registers for z[n] and the moments, so the request relaxes with n.
+#ifndef HJMC_MINB
+#define HJMC_MINB 0
+#endif
+template <int NDIM>
+constexpr int min_blocks() {
+  return HJMC_MINB > 0 ? HJMC_MINB : (NDIM <= 6 ? 4 : (NDIM <= 16 ? 2 : 1));
+}
+
 template <class Tgt, int NDIM, int NT>
-__global__ void __launch_bounds__(NT) solve_kernel(const __grid_constant__ SolveParams P) {
+__global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __grid_constant__ SolveParams P) {
   __shared__ SolveSmem<NDIM, NT> sm;
   const int64_t unit = blockIdx.x;
   int64_t m;
@@ -216,6 +231,7 @@ __global__ void __launch_bounds__(NT) solve_kernel(const __grid_constant__ Solve
   const double tau = (P.mode == kModeSolve) ? (double)j * P.T / (double)P.K : P.tau_vg;
   const double sigma_d = sqrt(P.gp.delta_eff * tau);
   const float sigma = (float)sigma_d;
+  const float sigma_s = (float)(sigma_d * (double)kBMScale);  // y = x + σ z = x + (σC) ẑ
   float xs[NDIM];
 #pragma unroll
   for (int d = 0; d < NDIM; ++d) {
@@ -249,14 +265,14 @@ __global__ void __launch_bounds__(NT) solve_kernel(const __grid_constant__ Solve
     float B = -A * lowc;  // every a_i = A core_i + B ≤ 0: no weight can overflow
 
     float S, Mz[NDIM];
-    mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma, A, B, P.N, P.antithetic, w1base, id, P.tag,
-                                 P.key, S, Mz);
+    mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id, P.tag,
+                                 P.rk, S, Mz);
     cta_reduce<NDIM, NT>(sm, S, Mz);
     if (!(sm.sum[0] >= (double)kUnderflowS)) {
       // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with
       // the exact maximum exponent, the plain two-pass log-sum-exp.
       const float amax = warp_max(mc_max_exponent<Tgt, NDIM, NT>(
-          tgt, xs, sigma, A, P.N, P.antithetic, w1base, id, P.tag, P.key));
+          tgt, xs, sigma_s, A, P.N, P.antithetic, w1base, id, P.tag, P.rk));
       if ((threadIdx.x & 31) == 0) sm.fmax_part[threadIdx.x >> 5] = amax;
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -266,8 +282,8 @@ __global__ void __launch_bounds__(NT) solve_kernel(const __grid_constant__ Solve
       }
       __syncthreads();
       B = -sm.shift;
-      mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma, A, B, P.N, P.antithetic, w1base, id, P.tag,
-                                   P.key, S, Mz);
+      mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id, P.tag,
+                                   P.rk, S, Mz);
       cta_reduce<NDIM, NT>(sm, S, Mz);
     }
     if (threadIdx.x == 0)
@@ -312,7 +328,7 @@ cudaError_t launch_eval_target(const EvalParams& p, cudaStream_t s) {
 // One instantiation set per (target, n): the fused solve kernel and the g/Dg evaluator.
 template <template <int> class T, int NDIM>
 KernelSet make_set() {
-  constexpr int kThreads = 256;
+  constexpr int kThreads = HJMC_NT;
   KernelSet k;
   k.solve = &launch_solve<T<NDIM>, NDIM, kThreads>;
   k.eval_target = &launch_eval_target<T<NDIM>, NDIM>;

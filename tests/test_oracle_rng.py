@@ -94,7 +94,7 @@ def test_uniform_mapping_from_raw_words(oracle_mod):
     """z from the raw Philox words per the header's prose (consistency, not a pin)."""
     P = oracle_mod.Problem(n=4, seed=5)
     z, raw = oracle_mod.normals(P, 9, 2, 0, 0, 64, raw=True)
-    m = (raw & 0x7FFFFF).astype(np.float64)
+    m = (raw >> 9).astype(np.float64)
     u = (2 * m + 1) / 2**24
     a = m / 2**23
     r0 = np.sqrt(-2 * np.log(u[:, 0]))

@@ -11,7 +11,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import oracle as O  # noqa: E402
-from _parity import dv_violations, v_violations  # noqa: E402
+from _parity import c_violations, dv_violations, v_violations  # noqa: E402
 from paper_2605_18566_b200 import inputs as I  # noqa: E402
 from paper_2605_18566_b200.solver import Solver, SolverConfig  # noqa: E402
 
@@ -29,11 +29,17 @@ def report(name, preset, x, qids=None):
     vr = max(v_violations(g["vhist"][j, k], ref["vhist"][j, k]).max() for j in range(K) for k in range(Kp))
     cr = max(v_violations(g["chist"][j, k], ref["chist"][j, k]).max() for j in range(K) for k in range(Kp))
     crel = max(np.abs(g["chist"][j, k] / ref["chist"][j, k] - 1).max() for j in range(K) for k in range(Kp))
+    P = O.Problem.from_preset(preset)
+    xs = x if qids is None else x[qids]
+    dg = np.stack([O.dg(P, xm.astype(np.float64)) for xm in xs])
+    cb = max(c_violations(O, P, xs, g["chist"][j, k], ref["chist"][j, k],
+                          dg if k == 0 else ref["dvhist"][j, k - 1]).max()
+             for j in range(K) for k in range(Kp))
     interior = ((ref["chist"] > preset.c_min * 1.001) & (ref["chist"] < preset.c_max * 0.999)).mean()
     print(f"{name:28s} M={x.shape[0] if qids is None else len(qids):6d} "
           f"vhist {vr:7.3f}  v {v_violations(g['v'], ref['v']).max():7.3f}  "
           f"dv {dv_violations(g['dv'], ref['dv']).max():7.3f}  tube {v_violations(g['tube'], ref['tube']).max():7.3f}  "
-          f"| chist {cr:7.3f} (max rel {crel:.2e}, interior frac {interior:.3f})", flush=True)
+          f"| chist {cr:7.3f} (max rel {crel:.2e}, interior frac {interior:.3f}; perturbation-bound ratio {cb:.3f})", flush=True)
 
 
 def grid(lo, hi, pts, fixed):
