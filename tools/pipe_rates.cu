@@ -1,97 +1,148 @@
 // pipe_rates.cu — sm_100a per-pipe throughput microbenchmark (lane-ops per SM clock).
-// Each thread runs 8 independent dependency chains of one instruction class; 4 CTAs × 256
-// threads per SM keep every SMSP saturated; each CTA times itself with clock64(). The result
-// (JSON on stdout) supplies the measured roofline denominators (profiles/pipe_rates.json).
-#include <cstdio>
-#include <cstdint>
-#include <vector>
-#include <algorithm>
+//
+// Each thread runs 8 independent dependency chains of one instruction form; 4 CTAs × 256
+// threads per SM saturate every SMSP. Every CTA records its SM id and clock64() at start and
+// end; per SM, rate = (lane-ops of all CTAs that ran there) / (last end − first start), and the
+// median over SMs is reported. The SASS of each loop body is listed in profiles/pipe_rates.md.
+// Output: JSON on stdout (the measured roofline denominators, profiles/pipe_rates.json).
 #include <cuda_runtime.h>
 
-constexpr int kIters = 4096;
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <vector>
+
+constexpr int kIters = 2048;
 constexpr int kChains = 8;
 
-#define DEFINE_BENCH(NAME, TYPE, INIT, BODY, OPS_PER_BODY)                                  \
-  __global__ void NAME(TYPE* out, long long* cyc, TYPE p0, TYPE p1, TYPE p2) {              \
-    TYPE v[kChains];                                                                        \
-    for (int c = 0; c < kChains; ++c) v[c] = INIT;                                          \
-    __syncthreads();                                                                        \
-    long long t0 = clock64();                                                               \
-    for (int it = 0; it < kIters; ++it) {                                                   \
-      _Pragma("unroll") for (int c = 0; c < kChains; ++c) { BODY; }                         \
-    }                                                                                       \
-    __syncthreads();                                                                        \
-    long long t1 = clock64();                                                               \
-    TYPE acc = v[0];                                                                        \
-    for (int c = 1; c < kChains; ++c) acc = acc + v[c];                                     \
-    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;                                       \
-    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;                                        \
+struct Stamp {
+  long long t0, t1;
+  unsigned smid;
+};
+
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+#define DEFINE_BENCH(NAME, TYPE, INIT, BODY)                                              \
+  __global__ void NAME(TYPE* out, Stamp* st, TYPE p0, TYPE p1, TYPE p2) {                 \
+    TYPE v[kChains];                                                                      \
+    for (int c = 0; c < kChains; ++c) v[c] = INIT;                                        \
+    __syncthreads();                                                                      \
+    long long t0 = clock64();                                                             \
+    for (int it = 0; it < kIters; ++it) {                                                 \
+      _Pragma("unroll") for (int c = 0; c < kChains; ++c) { BODY; }                       \
+    }                                                                                     \
+    __syncthreads();                                                                      \
+    long long t1 = clock64();                                                             \
+    TYPE acc = v[0];                                                                      \
+    for (int c = 1; c < kChains; ++c) acc = acc ^ v[c];                                   \
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;                                     \
+    if (threadIdx.x == 0) st[blockIdx.x] = Stamp{t0, t1, smid()};                         \
+  }
+
+#define DEFINE_FBENCH(NAME, INIT, BODY)                                                   \
+  __global__ void NAME(float* out, Stamp* st, float p0, float p1, float p2) {             \
+    float v[kChains];                                                                     \
+    for (int c = 0; c < kChains; ++c) v[c] = INIT;                                        \
+    __syncthreads();                                                                      \
+    long long t0 = clock64();                                                             \
+    for (int it = 0; it < kIters; ++it) {                                                 \
+      _Pragma("unroll") for (int c = 0; c < kChains; ++c) { BODY; }                       \
+    }                                                                                     \
+    __syncthreads();                                                                      \
+    long long t1 = clock64();                                                             \
+    float acc = v[0];                                                                     \
+    for (int c = 1; c < kChains; ++c) acc = acc + v[c];                                   \
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;                                     \
+    if (threadIdx.x == 0) st[blockIdx.x] = Stamp{t0, t1, smid()};                         \
   }
 
 __device__ __forceinline__ float ex2a(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float lg2a(float x) { float y; asm volatile("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float sqrta(float x) { float y; asm volatile("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
-__device__ __forceinline__ float sina(float x) { float y; asm volatile("sin.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float cosa(float x) { float y; asm volatile("cos.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
-DEFINE_BENCH(b_ffma, float, p0 + threadIdx.x * 1e-7f + c, v[c] = fmaf(v[c], p1, p2), 1)
-DEFINE_BENCH(b_fmul, float, p0 + threadIdx.x * 1e-7f + c, v[c] = v[c] * p1, 1)
-DEFINE_BENCH(b_lop3, uint32_t, p0 + threadIdx.x + c, v[c] = v[c] ^ p1 ^ (v[c] >> 3), 2)
+// FP32
+DEFINE_FBENCH(b_ffma, p0 + threadIdx.x * 1e-7f + c, v[c] = fmaf(v[c], p1, p2))
+DEFINE_FBENCH(b_fadd, p0 + threadIdx.x * 1e-7f + c, v[c] = v[c] + p1)
+// integer multiply forms (each body: the multiply + one LOP3 on the ALU pipe to keep values moving)
+DEFINE_BENCH(b_imad_wide, uint32_t, (uint32_t)p0 + threadIdx.x + c,
+             { uint32_t hi = __umulhi(v[c], 0xD2511F53u); v[c] = (v[c] * 0xD2511F53u) ^ hi; })
+DEFINE_BENCH(b_imad_lo, uint32_t, (uint32_t)p0 + threadIdx.x + c, v[c] = v[c] * 0xD2511F53u + p1)
+DEFINE_BENCH(b_imad_hi, uint32_t, (uint32_t)p0 + threadIdx.x + c,
+             v[c] = __umulhi(v[c], 0xD2511F53u) ^ (p1 + c))
+// logic (ALU pipe): 3-input XOR chains across neighbouring chains
+DEFINE_BENCH(b_lop3, uint32_t, (uint32_t)p0 + threadIdx.x * 7u + c,
+             v[c] = v[c] ^ v[(c + 3) % kChains] ^ (p1 + c))
+// MUFU (XU pipe)
+DEFINE_FBENCH(b_ex2, p0 + threadIdx.x * 1e-6f + c * 1e-3f, v[c] = ex2a(-v[c]))
+DEFINE_FBENCH(b_sqrt, p0 + 2.0f + threadIdx.x * 1e-3f + c, v[c] = sqrta(v[c]))
+DEFINE_FBENCH(b_lg2, p0 + 2.0f + threadIdx.x * 1e-3f + c, v[c] = lg2a(v[c]) + p1)
+DEFINE_FBENCH(b_cos, p0 + threadIdx.x * 1e-6f + c * 1e-3f, v[c] = cosa(v[c]))
 
-DEFINE_BENCH(b_imulwide, uint32_t, p0 + threadIdx.x + c,
-             { uint32_t hi = __umulhi(v[c], 0xD2511F53u); v[c] = (v[c] * 0xD2511F53u) ^ hi; }, 1)
-DEFINE_BENCH(b_ex2, float, p0 + threadIdx.x * 1e-6f + c * 1e-3f, v[c] = ex2a(-v[c]), 1)
-DEFINE_BENCH(b_sqrt, float, p0 + 2.0f + threadIdx.x * 1e-3f + c, v[c] = sqrta(v[c]), 1)
-DEFINE_BENCH(b_sin, float, p0 + threadIdx.x * 1e-6f + c * 1e-3f, v[c] = sina(v[c]), 1)
-DEFINE_BENCH(b_lg2, float, p0 + 2.0f + threadIdx.x * 1e-3f + c, v[c] = lg2a(v[c]) + p1, 1)
+struct Result {
+  const char* name;
+  const char* pipe;
+  double lane_ops_per_clk;
+};
 
 template <typename T>
-double run(void (*k)(T*, long long*, T, T, T), T p0, T p1, T p2, int nsm, const char* name,
-           double ops_per_body, cudaEvent_t e0, cudaEvent_t e1, float* ms_out) {
-  const int ctas_per_sm = 4, threads = 256;
-  const int grid = nsm * ctas_per_sm;
-  T* out; long long* cyc;
-  cudaMalloc(&out, sizeof(T) * grid * threads);
-  cudaMalloc(&cyc, sizeof(long long) * grid);
-  k<<<grid, threads>>>(out, cyc, p0, p1, p2);  // warm
-  cudaEventRecord(e0);
-  k<<<grid, threads>>>(out, cyc, p0, p1, p2);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  cudaEventElapsedTime(ms_out, e0, e1);
-  std::vector<long long> h(grid);
-  cudaMemcpy(h.data(), cyc, sizeof(long long) * grid, cudaMemcpyDeviceToHost);
-  std::sort(h.begin(), h.end());
-  const double med = (double)h[grid / 2];
-  // ops per SM during one CTA's lifetime: 4 concurrent CTAs × threads × iters × chains × ops
-  const double ops = (double)ctas_per_sm * threads * kIters * kChains * ops_per_body;
-  cudaFree(out); cudaFree(cyc);
-  return ops / med;
+double run(void (*k)(T*, Stamp*, T, T, T), T p0, T p1, T p2, int nsm) {
+  const int ctas = nsm * 4, threads = 256;
+  T* out;
+  Stamp* st;
+  cudaMalloc(&out, sizeof(T) * ctas * threads);
+  cudaMalloc(&st, sizeof(Stamp) * ctas);
+  k<<<ctas, threads>>>(out, st, p0, p1, p2);  // warm-up
+  k<<<ctas, threads>>>(out, st, p0, p1, p2);
+  cudaDeviceSynchronize();
+  std::vector<Stamp> h(ctas);
+  cudaMemcpy(h.data(), st, sizeof(Stamp) * ctas, cudaMemcpyDeviceToHost);
+  std::map<unsigned, std::vector<Stamp>> by;
+  for (auto& s : h) by[s.smid].push_back(s);
+  std::vector<double> rates;
+  const double ops_per_cta = (double)threads * kIters * kChains;  // one op per body
+  for (auto& kv : by) {
+    long long lo = kv.second[0].t0, hi = kv.second[0].t1;
+    for (auto& s : kv.second) { lo = std::min(lo, s.t0); hi = std::max(hi, s.t1); }
+    rates.push_back(ops_per_cta * kv.second.size() / (double)(hi - lo));
+  }
+  std::sort(rates.begin(), rates.end());
+  cudaFree(out);
+  cudaFree(st);
+  return rates[rates.size() / 2];
 }
 
 int main() {
-  int dev = 0, nsm = 0, clk = 0;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0); cudaEventCreate(&e1);
-  float ms;
-  printf("{\n  \"device_sms\": %d, \"clock_rate_khz\": %d,\n  \"raw\": {\n", nsm, clk);
-  struct R { const char* n; double r; float ms; };
-  std::vector<R> rs;
-  rs.push_back({"ffma", run<float>(b_ffma, 1.0f, 0.999f, 1e-6f, nsm, "ffma", 1, e0, e1, &ms), ms});
-  rs.push_back({"fmul", run<float>(b_fmul, 1.0f, 0.99999f, 0.f, nsm, "fmul", 1, e0, e1, &ms), ms});
-  rs.push_back({"lop3_shift", run<uint32_t>(b_lop3, 1u, 0x9E3779B9u, 0u, nsm, "lop3", 2, e0, e1, &ms), ms});
-
-  rs.push_back({"imul_wide_plus_xor", run<uint32_t>(b_imulwide, 1u, 0u, 0u, nsm, "imulwide", 1, e0, e1, &ms), ms});
-  rs.push_back({"mufu_ex2", run<float>(b_ex2, 0.5f, 0.f, 0.f, nsm, "ex2", 1, e0, e1, &ms), ms});
-  rs.push_back({"mufu_sqrt", run<float>(b_sqrt, 0.f, 0.f, 0.f, nsm, "sqrt", 1, e0, e1, &ms), ms});
-  rs.push_back({"mufu_sin", run<float>(b_sin, 0.5f, 0.f, 0.f, nsm, "sin", 1, e0, e1, &ms), ms});
-  rs.push_back({"mufu_lg2_plus_fadd", run<float>(b_lg2, 0.f, 2.0f, 0.f, nsm, "lg2", 1, e0, e1, &ms), ms});
-  for (size_t i = 0; i < rs.size(); ++i)
-    printf("    \"%s\": {\"lane_ops_per_clk_per_sm\": %.3f, \"ms\": %.4f}%s\n", rs[i].n, rs[i].r,
-           rs[i].ms, i + 1 < rs.size() ? "," : "");
-  printf("  }\n}\n");
+  int nsm = 0, clk = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  std::vector<Result> r;
+  r.push_back({"ffma", "fp32", run<float>(b_ffma, 1.0f, 0.999f, 1e-6f, nsm)});
+  r.push_back({"fadd", "fp32", run<float>(b_fadd, 1.0f, 1e-7f, 0.f, nsm)});
+  r.push_back({"imad_wide_u32 (+lop3)", "imul", run<uint32_t>(b_imad_wide, 1u, 0u, 0u, nsm)});
+  r.push_back({"imad_lo", "imad_lo", run<uint32_t>(b_imad_lo, 1u, 0x9E3779B9u, 0u, nsm)});
+  r.push_back({"imad_hi (+lop3)", "imad_hi", run<uint32_t>(b_imad_hi, 1u, 0x9E3779B9u, 0u, nsm)});
+  r.push_back({"lop3", "alu", run<uint32_t>(b_lop3, 1u, 0x9E3779B9u, 0u, nsm)});
+  r.push_back({"mufu_ex2", "mufu", run<float>(b_ex2, 0.5f, 0.f, 0.f, nsm)});
+  r.push_back({"mufu_sqrt", "mufu_sqrt", run<float>(b_sqrt, 0.f, 0.f, 0.f, nsm)});
+  r.push_back({"mufu_lg2 (+fadd)", "mufu_lg2", run<float>(b_lg2, 0.f, 2.0f, 0.f, nsm)});
+  r.push_back({"mufu_cos (+fmul.rz)", "mufu_cos", run<float>(b_cos, 0.5f, 0.f, 0.f, nsm)});
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) { fprintf(stderr, "CUDA error %s\n", cudaGetErrorString(e)); return 1; }
+  if (e != cudaSuccess) {
+    fprintf(stderr, "CUDA error %s\n", cudaGetErrorString(e));
+    return 1;
+  }
+  printf("{\n  \"device_sms\": %d, \"clock_rate_khz\": %d,\n", nsm, clk);
+  printf("  \"method\": \"per-SM clock64 window over 4 CTAs x 256 threads x 8 chains; median over SMs\",\n");
+  printf("  \"raw\": {\n");
+  for (size_t i = 0; i < r.size(); ++i)
+    printf("    \"%s\": {\"pipe\": \"%s\", \"lane_ops_per_clk_per_sm\": %.3f}%s\n", r[i].name,
+           r[i].pipe, r[i].lane_ops_per_clk, i + 1 < r.size() ? "," : "");
+  printf("  }\n}\n");
   return 0;
 }
