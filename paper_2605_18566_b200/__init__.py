@@ -15,12 +15,10 @@ __all__ = ["Solver", "SolverConfig", "residual_partials", "supported", "inputs",
 
 
 def __getattr__(name):
+    import importlib
+
     if name in ("Solver", "SolverConfig", "residual_partials", "supported"):
-        from . import solver
-
-        return getattr(solver, name)
-    if name == "shard":
-        from . import shard
-
-        return shard
+        return getattr(importlib.import_module(__name__ + ".solver"), name)
+    if name in ("shard", "roofline", "solver", "build"):
+        return importlib.import_module(__name__ + "." + name)
     raise AttributeError(name)

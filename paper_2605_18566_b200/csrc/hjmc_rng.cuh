@@ -106,6 +106,20 @@ __device__ __forceinline__ uint32_t ctr_word1(uint32_t b, uint32_t kw, uint32_t 
   return b | (kw << 8) | (jw << 16);
 }
 
+// ẑ of one quad from its Philox words (the first min(NDIM, 4) coordinates).
+template <int NDIM>
+__device__ __forceinline__ void quad_normals_hat(float (&z)[NDIM], uint4 w) {
+  float t0, t1, t2, t3;
+  box_muller_hat<(NDIM >= 2)>(w.x, w.y, t0, t1);
+  z[0] = t0;
+  if constexpr (NDIM >= 2) z[1] = t1;
+  if constexpr (NDIM >= 3) {
+    box_muller_hat<(NDIM >= 4)>(w.z, w.w, t2, t3);
+    z[2] = t2;
+    if constexpr (NDIM >= 4) z[3] = t3;
+  }
+}
+
 // ẑ (= z / C) of draw `draw` (= sample index, or index >> 1 under antithetic sampling).
 template <int NDIM>
 __device__ __forceinline__ void sample_normals_hat(float (&z)[NDIM], uint32_t draw, uint32_t w1base,

@@ -19,8 +19,16 @@
 
 namespace hjmc {
 
+#ifndef HJMC_SWP
+#define HJMC_SWP 0
+#endif
+#ifndef HJMC_UNROLL
+#define HJMC_UNROLL 2
+#endif
+
 namespace {
 
+constexpr int kSampleUnroll = HJMC_UNROLL;
 constexpr double kLog2e = 1.4426950408889634074;
 constexpr double kLn2 = 0.69314718055994530942;
 constexpr float kUnderflowS = 7.888609052210118e-31f;  // 2^-100: fallback threshold
@@ -47,7 +55,23 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
 #pragma unroll
   for (int d = 0; d < NDIM; ++d) Mz[d] = 0.f;
   if (!antithetic) {
-#pragma unroll 2
+    if constexpr (HJMC_SWP && NDIM <= 4) {
+    // Software-pipelined: the Philox words of the next sample (integer multiply + logic pipes)
+    // are produced while this sample's Box–Muller, target and moments (MUFU + FP32 pipes) run.
+    uint32_t i = threadIdx.x;
+    uint4 w = philox4x32_10(i, w1base, qid, tag, rk);
+    for (; i < N; i += NT) {
+      const uint4 wc = w;
+      if (i + NT < N) w = philox4x32_10(i + NT, w1base, qid, tag, rk);
+      float z[NDIM];
+      quad_normals_hat<NDIM>(z, wc);
+      const float wt = ex2_approx(fmaf(A, tgt.core(xs, sigma, z), B));
+      S += wt;
+#pragma unroll
+      for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(wt, z[d], Mz[d]);
+    }
+    } else {
+#pragma unroll kSampleUnroll
     for (uint32_t i = threadIdx.x; i < N; i += NT) {
       float z[NDIM];
       sample_normals_hat<NDIM>(z, i, w1base, qid, tag, rk);
@@ -55,6 +79,7 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
       S += w;
 #pragma unroll
       for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(w, z[d], Mz[d]);
+    }
     }
   } else {
     const uint32_t draws = (N >> 1) + (N & 1u);

@@ -8,11 +8,13 @@ sys.path.insert(0, ROOT)
 from paper_2605_18566_b200 import build as B  # noqa: E402
 
 VARIANTS = {
-    "nt256_mb1": ["-DHJMC_NT=256", "-DHJMC_MINB=1"],
-    "nt256_mb3": ["-DHJMC_NT=256", "-DHJMC_MINB=3"],
-    "nt256_mb4": ["-DHJMC_NT=256", "-DHJMC_MINB=4"],
-    "nt128_mb8": ["-DHJMC_NT=128", "-DHJMC_MINB=8"],
-    "nt512_mb2": ["-DHJMC_NT=512", "-DHJMC_MINB=2"],
+    "a_base": [],
+    "b_swp": ["-DHJMC_SWP=1"],
+    "c_unroll1": ["-DHJMC_UNROLL=1"],
+    "d_unroll4": ["-DHJMC_UNROLL=4"],
+    "e_mb5": ["-DHJMC_MINB=5"],
+    "f_swp_mb5": ["-DHJMC_SWP=1", "-DHJMC_MINB=5"],
+    "g_nt128": ["-DHJMC_NT=128", "-DHJMC_MINB=8"],
 }
 
 if __name__ == "__main__":
@@ -22,6 +24,6 @@ if __name__ == "__main__":
         B.build(force=True, extra=VARIANTS[name], out=out,
                 obj_dir=os.path.join(ROOT, "variants", "_obj_" + name))
         return out
-    with ThreadPoolExecutor(2) as ex:
+    with ThreadPoolExecutor(3) as ex:
         for o in ex.map(one, names):
             print(o)
