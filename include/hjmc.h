@@ -134,6 +134,11 @@ extern "C" {
 
 /* Config flags. */
 #define HJMC_FLAG_SYNC_CHECK 1u
+/* With crn = 1: when Γ returns exactly the coefficient just used, every remaining Picard iterate
+ * of that (query, horizon) has bit-identical inputs and therefore bit-identical outputs; they
+ * are copied instead of recomputed (Algorithm 1's convergence test at ε = 0, per query).
+ * Outputs are identical with and without the flag; hjmc_pass_count() reports the work done. */
+#define HJMC_FLAG_SKIP_STATIONARY 2u
 
 /* Systems (Hamiltonians). */
 #define HJMC_SYS_QUADRATIC 0
@@ -233,6 +238,27 @@ HJMC_API int hjmc_solve_slice(hjmc_handle* h, const float* x, const uint32_t* qi
 HJMC_API int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, uint32_t qid_base, int64_t M,
                           const float* drift_host, const hjmc_result* out_host);
 
+/* ---- Stepwise Picard: Algorithm 1 with its convergence test (step 5) ------------
+ * The fused solve runs a fixed Kp. Algorithm 1 instead stops when
+ *   ε_j(k) = ‖v^(k+1) − v^(k)‖₂ / ‖v^(k)‖₂ < ε     (norms over the slice's queries, R11),
+ * a slice-wide (and, sharded, cross-GPU) quantity. The caller drives it:
+ *   hjmc_picard_begin  — v^(0) = g(x), c^(0) = Γ(x, Dg(x)) for every horizon (handle state);
+ *                        x / qid / drift must stay valid until the last pass.
+ *   hjmc_picard_pass   — one Φ pass (iterate k) for every horizon with active[j] != 0 (NULL =
+ *                        all): v (dev [K][M]), dv (dev [K][M][n]) and c (dev [K][M], the
+ *                        updated Γ(x, Dv)) are written for active rows (each may be NULL);
+ *                        partials (HOST [K][3]) receives per horizon (Σ(v^(k+1)−v^(k))²,
+ *                        Σ(v^(k))², max|v^(k+1)−v^(k)|) over this handle's queries, zeros for
+ *                        inactive horizons. Synchronises the stream. Sum the first two and take
+ *                        the max of the third across shards, then ε_j(k) = sqrt(num/den) and
+ *                        Theorem 2's sup-norm differences. Iterates run with the
+ *                        same counters as hjmc_solve_slice, so with every horizon active for
+ *                        Kp passes the v rows equal vhist[·][k] bit for bit. */
+HJMC_API int hjmc_picard_begin(hjmc_handle* h, const float* x, const uint32_t* qid,
+                               uint32_t qid_base, int64_t M, const float* drift, void* stream);
+HJMC_API int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, float* v,
+                              float* dv, float* c, double* partials, void* stream);
+
 /* g(x) and the analytic Dg(x) used for c^(0) (dev pointers; dg may be NULL). */
 HJMC_API int hjmc_eval_target(hjmc_handle* h, const float* x, int64_t M, float* g, float* dg,
                      void* stream);
@@ -250,6 +276,10 @@ HJMC_API int hjmc_debug_normals(hjmc_handle* h, uint32_t qid, uint32_t jw, uint3
 /* Synchronise stream, then return HJMC_ENUMERIC if any earlier call on this handle produced
  * a non-finite value (clearing the flag), else HJMC_OK. */
 HJMC_API int hjmc_check(hjmc_handle* h, void* stream);
+
+/* Number of Φ passes (each N samples of one query) the device executed since the previous call
+ * (synchronises stream). Without HJMC_FLAG_SKIP_STATIONARY a solve_slice executes M·K·Kp. */
+HJMC_API int hjmc_pass_count(hjmc_handle* h, void* stream, uint64_t* passes);
 
 /* Smallest global query id that failed numerically since the last hjmc_check, or −1. */
 HJMC_API int64_t hjmc_last_bad_query(const hjmc_handle* h);

@@ -68,6 +68,9 @@ def lib():
                                       dp, dp, dp, C.c_int32]
         L.orc_solve_slice.restype = C.c_int
         L.orc_residual_partials.argtypes = [dp, dp, C.c_int32, C.c_int32, C.c_int64, dp]
+        L.orc_picard_adaptive.argtypes = [pp, fp, up, C.c_uint32, C.c_int64, C.c_double, C.c_int32,
+                                          dp, dp, dp, dp, C.c_int32]
+        L.orc_picard_adaptive.restype = C.c_int
         L.orc_max_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -225,6 +228,24 @@ def solve_slice(P: Problem, x, drift=None, qid_base: int = 0, qids=None, nthread
         _dp(out["vhist"]), _dp(out["chist"]), _dp(out["g0"]), _dp(out["dvhist"]), nthreads)
     out["status"] = st
     return out
+
+
+def picard_adaptive(P: Problem, x, tol: float, max_iter: int, qid_base: int = 0, qids=None,
+                    nthreads: int = 0):
+    """Algorithm 1 with the convergence test, per horizon. Returns v [K][M], iters [K],
+    eps [K][max_iter], d_sup [K][max_iter]."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    M, K = x.shape[0], P.K
+    v = np.zeros((K, M))
+    iters = np.zeros(K)
+    eps = np.zeros((K, max_iter))
+    dsup = np.zeros((K, max_iter))
+    q = None if qids is None else np.ascontiguousarray(qids, dtype=np.uint32)
+    st = lib().orc_picard_adaptive(C.byref(P.struct()), x.ctypes.data_as(C.POINTER(C.c_float)),
+                                   q.ctypes.data_as(C.POINTER(C.c_uint32)) if q is not None else None,
+                                   qid_base, M, tol, max_iter, _dp(v), _dp(iters), _dp(eps),
+                                   _dp(dsup), nthreads)
+    return {"v": v, "iters": iters.astype(int), "eps": eps, "d_sup": dsup, "status": st}
 
 
 def gamma_sensitivity(P: Problem, x, p, rel: float = 1e-6) -> float:

@@ -378,6 +378,76 @@ int orc_solve_slice(const orc_problem* P, const float* x, const float* drift, co
   return status;
 }
 
+/* Algorithm 1 WITH its convergence test (step 5): for each horizon j, v^(0) = g,
+ * c^(0) = Gamma(x, Dg); repeat for all queries: Phi at frozen c, then
+ * eps = ||v^(k+1) - v^(k)||_2 / ||v^(k)||_2 over the M queries (R11), c <- Gamma(x, Dv);
+ * stop when eps < tol or after max_iter passes. Outputs (caller-sized): v [K][M] (final
+ * iterate), iters [K], eps and dsup [K][max_iter] (NAN after the stop; dsup = sup-norm of the
+ * difference, Theorem 2's quantity). */
+int orc_picard_adaptive(const orc_problem* P, const float* x, const uint32_t* qid,
+                        uint32_t qid_base, int64_t M, double tol, int32_t max_iter, double* v_out,
+                        double* iters, double* eps, double* dsup, int32_t nthreads) {
+  int n = P->n, K = P->K;
+  double* vprev = (double*)malloc(sizeof(double) * (size_t)M);
+  double* vcur = (double*)malloc(sizeof(double) * (size_t)M);
+  double* c = (double*)malloc(sizeof(double) * (size_t)M);
+  if (!vprev || !vcur || !c) { free(vprev); free(vcur); free(c); return 1; }
+  int status = 0;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+  for (int j = 1; j <= K; ++j) {
+    double tau = (double)j * P->T / (double)K;
+    for (int64_t m = 0; m < M; ++m) {         /* v^(0) = g, c^(0) = Gamma(x, Dg) */
+      double xm[ORC_MAX_N], dg[ORC_MAX_N];
+      for (int d = 0; d < n; ++d) xm[d] = (double)x[m * n + d];
+      vprev[m] = orc_target_g(P, xm);
+      orc_target_dg(P, xm, dg);
+      c[m] = orc_gamma(P, xm, dg);
+    }
+    for (int k = 0; k < max_iter; ++k) {
+      eps[(size_t)(j - 1) * max_iter + k] = NAN;
+      dsup[(size_t)(j - 1) * max_iter + k] = NAN;
+    }
+    int k;
+    for (k = 0; k < max_iter; ++k) {
+      uint32_t kw = P->crn ? 0u : (uint32_t)k;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic, 1)
+#endif
+      for (int64_t m = 0; m < M; ++m) {
+        double xm[ORC_MAX_N], dvm[ORC_MAX_N];
+        for (int d = 0; d < n; ++d) xm[d] = (double)x[m * n + d];
+        uint32_t id = qid ? qid[m] : qid_base + (uint32_t)m;
+        int st = orc_phi(P, xm, NULL, id, c[m], tau, (uint32_t)j, kw, &vcur[m], dvm, NULL, NULL);
+        if (st) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+          status = st;
+        }
+        c[m] = orc_gamma(P, xm, dvm);
+      }
+      double num = 0.0, den = 0.0, mx = 0.0;
+      for (int64_t m = 0; m < M; ++m) {
+        double d = vcur[m] - vprev[m];
+        num += d * d;
+        den += vprev[m] * vprev[m];
+        if (fabs(d) > mx) mx = fabs(d);
+        vprev[m] = vcur[m];
+      }
+      double e = sqrt(num / den);
+      eps[(size_t)(j - 1) * max_iter + k] = e;
+      dsup[(size_t)(j - 1) * max_iter + k] = mx;
+      if (e < tol) { ++k; break; }
+    }
+    iters[j - 1] = (double)k;
+    for (int64_t m = 0; m < M; ++m) v_out[(size_t)(j - 1) * M + m] = vprev[m];
+  }
+  free(vprev); free(vcur); free(c);
+  return status;
+}
+
 /* Picard residual partial sums (relative L2 over the slice, R11), v^(0) = g. */
 void orc_residual_partials(const double* vhist, const double* g0, int32_t K, int32_t Kp,
                            int64_t M, double* out) {

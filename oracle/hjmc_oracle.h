@@ -71,6 +71,9 @@ int orc_phi(const orc_problem* P, const double* x, const double* drift, uint32_t
 int orc_solve_slice(const orc_problem* P, const float* x, const float* drift, const uint32_t* qid,
                     uint32_t qid_base, int64_t M, double* v, double* dv, double* c, double* tube,
                     double* vhist, double* chist, double* g0, double* dvhist, int32_t nthreads);
+int orc_picard_adaptive(const orc_problem* P, const float* x, const uint32_t* qid,
+                        uint32_t qid_base, int64_t M, double tol, int32_t max_iter, double* v_out,
+                        double* iters, double* eps, double* dsup, int32_t nthreads);
 void orc_residual_partials(const double* vhist, const double* g0, int32_t K, int32_t Kp,
                            int64_t M, double* out);
 int orc_max_threads(void);

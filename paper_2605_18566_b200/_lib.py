@@ -17,12 +17,14 @@ SYSTEMS = {"quadratic": 0, "dubins_rel": 1, "rocket6": 2, "dubins_pairs": 3}
 TARGETS = {"quad_bowl": 0, "disk": 1, "rel_disk6": 2, "pair_union": 3, "linear": 4, "const": 5}
 VISC = {"paper": 0, "full": 1}
 FLAG_SYNC_CHECK = 1
+FLAG_SKIP_STATIONARY = 2
 
 EXPORTS = [
     "hjmc_config_defaults", "hjmc_create", "hjmc_destroy", "hjmc_set_dynamics", "hjmc_set_target",
     "hjmc_supported", "hjmc_value_grad", "hjmc_solve_slice", "hjmc_solve_slice_host",
     "hjmc_eval_target", "hjmc_eval_hamiltonian", "hjmc_debug_normals", "hjmc_check",
     "hjmc_last_bad_query", "hjmc_last_error", "hjmc_residual_partials", "hjmc_version",
+    "hjmc_pass_count", "hjmc_picard_begin", "hjmc_picard_pass",
 ]
 
 
@@ -80,6 +82,9 @@ def load(path: str = LIB_PATH):
     L.hjmc_last_error.restype = C.c_char_p
     L.hjmc_residual_partials.argtypes = [vp, vp, C.c_int32, C.c_int32, i64, vp]
     L.hjmc_version.argtypes = []
+    L.hjmc_pass_count.argtypes = [vp, vp, C.POINTER(C.c_uint64)]
+    L.hjmc_picard_begin.argtypes = [vp, vp, vp, u32, i64, vp, vp]
+    L.hjmc_picard_pass.argtypes = [vp, C.c_int32, vp, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"libhjmc.so lacks {name}")

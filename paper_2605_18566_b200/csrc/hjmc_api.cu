@@ -6,7 +6,9 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <algorithm>
 #include <string>
+#include <vector>
 
 #include "../../include/hjmc.h"
 #include "hjmc_kernels.cuh"
@@ -23,6 +25,7 @@ struct hjmc_handle {
   KernelSet ks{};
   int* d_err = nullptr;
   unsigned long long* d_bad = nullptr;
+  unsigned long long* d_passes = nullptr;
   float* d_g0 = nullptr;
   size_t g0_cap = 0;
   float* d_vfinal = nullptr;
@@ -31,6 +34,21 @@ struct hjmc_handle {
   float* d_stage = nullptr;
   size_t stage_cap = 0;
   cudaStream_t host_stream = nullptr;
+  // stepwise Picard state (hjmc_picard_begin / hjmc_picard_pass)
+  const float* pic_x = nullptr;
+  const uint32_t* pic_qid = nullptr;
+  const float* pic_drift = nullptr;
+  uint32_t pic_qid_base = 0;
+  int64_t pic_M = -1;
+  double* d_cstate = nullptr;
+  size_t cstate_cap = 0;
+  float* d_vprev = nullptr;
+  size_t vprev_cap = 0;
+  float* d_vtmp = nullptr;
+  size_t vtmp_cap = 0;
+  int* d_active = nullptr;
+  double* d_partial = nullptr;
+  size_t partial_cap = 0;
   int64_t last_bad = -1;
   std::string err;
 };
@@ -86,6 +104,8 @@ void fill_common(const hjmc_handle* h, SolveParams* p) {
   p->tp = h->tp;
   p->err = h->d_err;
   p->bad = h->d_bad;
+  p->skip_stationary = (h->cfg.flags & HJMC_FLAG_SKIP_STATIONARY) ? 1 : 0;
+  p->passes = h->d_passes;
 }
 
 int ready(hjmc_handle* h) {
@@ -146,6 +166,8 @@ int hjmc_create(const hjmc_config* cfg, hjmc_handle** out) {
     return fail(nullptr, HJMC_EINVAL, "visc must be 0 or 1");
   if (c.crn != 0 && c.crn != 1) return fail(nullptr, HJMC_EINVAL, "crn must be 0 or 1");
   if (c.antithetic != 0 && c.antithetic != 1) return fail(nullptr, HJMC_EINVAL, "antithetic must be 0 or 1");
+  if (c.flags & ~(HJMC_FLAG_SYNC_CHECK | HJMC_FLAG_SKIP_STATIONARY))
+    return fail(nullptr, HJMC_EINVAL, "unknown flag bits");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess) return fail(nullptr, HJMC_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
@@ -158,6 +180,8 @@ int hjmc_create(const hjmc_config* cfg, hjmc_handle** out) {
       (e = cudaMalloc((void**)&h->d_bad, sizeof(unsigned long long))) != cudaSuccess ||
       (e = cudaMemset(h->d_err, 0, sizeof(int))) != cudaSuccess ||
       (e = cudaMemset(h->d_bad, 0xFF, sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaMalloc((void**)&h->d_passes, sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaMemset(h->d_passes, 0, sizeof(unsigned long long))) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&h->host_stream, cudaStreamNonBlocking)) != cudaSuccess) {
     std::string msg = std::string("device setup failed: ") + cudaGetErrorString(e);
     hjmc_destroy(h);
@@ -173,9 +197,15 @@ void hjmc_destroy(hjmc_handle* h) {
   cudaDeviceSynchronize();
   if (h->d_err) cudaFree(h->d_err);
   if (h->d_bad) cudaFree(h->d_bad);
+  if (h->d_passes) cudaFree(h->d_passes);
   if (h->d_g0) cudaFree(h->d_g0);
   if (h->d_vfinal) cudaFree(h->d_vfinal);
   if (h->d_stage) cudaFree(h->d_stage);
+  if (h->d_cstate) cudaFree(h->d_cstate);
+  if (h->d_vprev) cudaFree(h->d_vprev);
+  if (h->d_vtmp) cudaFree(h->d_vtmp);
+  if (h->d_active) cudaFree(h->d_active);
+  if (h->d_partial) cudaFree(h->d_partial);
   if (h->host_stream) cudaStreamDestroy(h->host_stream);
   delete h;
 }
@@ -388,6 +418,126 @@ int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, uint32_t qid_base
   return hjmc_check(h, (void*)s);
 }
 
+int hjmc_picard_begin(hjmc_handle* h, const float* x, const uint32_t* qid, uint32_t qid_base,
+                      int64_t M, const float* drift, void* stream) {
+  int rc = ready(h);
+  if (rc) return rc;
+  if (M < 1 || !x) return fail(h, HJMC_EINVAL, "need M >= 1 and x");
+  if (M * (int64_t)h->cfg.K > 0x7FFFFFFFLL) return fail(h, HJMC_EINVAL, "M*K exceeds 2^31-1");
+  if ((rc = set_device(h))) return rc;
+  const size_t KM = (size_t)M * (size_t)h->cfg.K;
+  if (KM > h->cstate_cap) {
+    if (h->d_cstate) cudaFree(h->d_cstate);
+    h->d_cstate = nullptr;
+    h->cstate_cap = 0;
+    cudaError_t e = cudaMalloc((void**)&h->d_cstate, KM * sizeof(double));
+    if (e != cudaSuccess) return fail(h, HJMC_ENOMEM, "picard state allocation failed");
+    h->cstate_cap = KM;
+  }
+  if ((rc = ensure(h, &h->d_vprev, &h->vprev_cap, KM))) return rc;
+  if (!h->d_active) {
+    cudaError_t e = cudaMalloc((void**)&h->d_active, 65536 * sizeof(int));
+    if (e != cudaSuccess) return fail(h, HJMC_ENOMEM, "picard active-list allocation failed");
+  }
+  h->pic_x = x;
+  h->pic_qid = qid;
+  h->pic_qid_base = qid_base;
+  h->pic_M = M;
+  h->pic_drift = drift;
+  PicardInitParams ip{};
+  ip.x = x;
+  ip.M = M;
+  ip.K = h->cfg.K;
+  ip.c_state = h->d_cstate;
+  ip.v_prev = h->d_vprev;
+  ip.gp.delta_eff = delta_eff(h->cfg);
+  ip.gp.m0 = h->cfg.m0;
+  ip.gp.c_min = h->cfg.c_min;
+  ip.gp.c_max = h->cfg.c_max;
+  ip.sp = h->sp;
+  ip.tp = h->tp;
+  cudaError_t e = h->ks.picard_init(ip, (cudaStream_t)stream);
+  return e == cudaSuccess ? HJMC_OK : cuda_fail(h, e, "picard init launch");
+}
+
+int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, float* v, float* dv,
+                     float* c, double* partials, void* stream) {
+  int rc = ready(h);
+  if (rc) return rc;
+  if (h->pic_M < 1) return fail(h, HJMC_EINVAL, "hjmc_picard_begin has not been called");
+  if (k < 0 || (!h->cfg.crn && k > 255)) return fail(h, HJMC_EINVAL, "bad iterate index k");
+  if (!partials) return fail(h, HJMC_EINVAL, "partials is required");
+  if ((rc = set_device(h))) return rc;
+  const int K = h->cfg.K;
+  const int64_t M = h->pic_M;
+  std::vector<int> act;
+  for (int j = 0; j < K; ++j)
+    if (!active || active[j]) act.push_back(j + 1);
+  for (int i = 0; i < 3 * K; ++i) partials[i] = 0.0;
+  if (act.empty()) return HJMC_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  float* vout = v;
+  if (!vout) {
+    if ((rc = ensure(h, &h->d_vtmp, &h->vtmp_cap, (size_t)M * (size_t)K))) return rc;
+    vout = h->d_vtmp;
+  }
+  const int blocks = (int)std::min<int64_t>(148, (M + 255) / 256);
+  const size_t need = act.size() * (size_t)blocks * 3;
+  if (need > h->partial_cap) {
+    if (h->d_partial) cudaFree(h->d_partial);
+    h->d_partial = nullptr;
+    h->partial_cap = 0;
+    if (cudaMalloc((void**)&h->d_partial, need * sizeof(double)) != cudaSuccess)
+      return fail(h, HJMC_ENOMEM, "picard partials allocation failed");
+    h->partial_cap = need;
+  }
+  cudaError_t e = cudaMemcpyAsync(h->d_active, act.data(), act.size() * sizeof(int),
+                                  cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "active list copy");
+  SolveParams p;
+  fill_common(h, &p);
+  p.x = h->pic_x;
+  p.drift = h->pic_drift;
+  p.qid = h->pic_qid;
+  p.qid_base = h->pic_qid_base;
+  p.M = M;
+  p.K = K;
+  p.Kp = 1;
+  p.T = (double)h->cfg.T;
+  p.mode = kModePass;
+  p.v = vout;
+  p.dv = dv;
+  p.c_out = c;
+  p.c_state = h->d_cstate;
+  p.active_j = h->d_active;
+  p.n_active = (int)act.size();
+  p.kiter = k;
+  p.skip_stationary = 0;
+  e = h->ks.solve(p, M * (int64_t)act.size(), s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "picard pass launch");
+  e = launch_picard_residual(vout, h->d_vprev, M, h->d_active, (int)act.size(), h->d_partial,
+                             blocks, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "picard residual launch");
+  std::vector<double> host(need);
+  e = cudaMemcpyAsync(host.data(), h->d_partial, need * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "picard partials read");
+  for (size_t a = 0; a < act.size(); ++a) {
+    double num = 0.0, den = 0.0, mx = 0.0;
+    for (int b = 0; b < blocks; ++b) {  // fixed order: deterministic
+      const double* q = host.data() + (a * (size_t)blocks + b) * 3;
+      num += q[0];
+      den += q[1];
+      mx = std::max(mx, q[2]);
+    }
+    double* o = partials + (size_t)(act[a] - 1) * 3;
+    o[0] = num;
+    o[1] = den;
+    o[2] = mx;
+  }
+  return sync_check_if_requested(h, s);
+}
+
 int hjmc_eval_target(hjmc_handle* h, const float* x, int64_t M, float* g, float* dg, void* stream) {
   if (!h) return HJMC_EINVAL;
   if (!h->tgt_set) return fail(h, HJMC_EINVAL, "hjmc_set_target has not been called");
@@ -463,6 +613,19 @@ int hjmc_check(hjmc_handle* h, void* stream) {
 }
 
 int64_t hjmc_last_bad_query(const hjmc_handle* h) { return h ? h->last_bad : -1; }
+
+int hjmc_pass_count(hjmc_handle* h, void* stream, uint64_t* passes) {
+  if (!h || !passes) return HJMC_EINVAL;
+  int rc = set_device(h);
+  if (rc) return rc;
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  unsigned long long v = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&v, h->d_passes, sizeof(v), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(h->d_passes, 0, sizeof(v));
+  if (e != cudaSuccess) return cuda_fail(h, e, "pass counter read");
+  *passes = (uint64_t)v;
+  return HJMC_OK;
+}
 
 const char* hjmc_last_error(const hjmc_handle* h) {
   return h ? h->err.c_str() : g_create_error.c_str();

@@ -54,7 +54,50 @@ __global__ void debug_normals_kernel(int n, uint32_t qid, uint32_t jw, uint32_t 
   }
 }
 
+__global__ void picard_residual_kernel(const float* __restrict__ v, float* __restrict__ v_prev,
+                                       int64_t M, const int* __restrict__ active_j,
+                                       double* __restrict__ partial) {
+  __shared__ double s_num[256], s_den[256], s_max[256];
+  const int a = blockIdx.y;
+  const size_t base = (size_t)(active_j[a] - 1) * (size_t)M;
+  double num = 0.0, den = 0.0, mx = 0.0;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < M;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const double cur = (double)v[base + m], prev = (double)v_prev[base + m];
+    const double d = cur - prev;
+    num += d * d;
+    den += prev * prev;
+    mx = fmax(mx, fabs(d));
+    v_prev[base + m] = v[base + m];
+  }
+  s_num[threadIdx.x] = num;
+  s_den[threadIdx.x] = den;
+  s_max[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      s_num[threadIdx.x] += s_num[threadIdx.x + o];
+      s_den[threadIdx.x] += s_den[threadIdx.x + o];
+      s_max[threadIdx.x] = fmax(s_max[threadIdx.x], s_max[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double* out = partial + ((size_t)a * gridDim.x + blockIdx.x) * 3;
+    out[0] = s_num[0];
+    out[1] = s_den[0];
+    out[2] = s_max[0];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_picard_residual(const float* v, float* v_prev, int64_t M, const int* active_j,
+                                   int n_active, double* partial, int blocks, cudaStream_t s) {
+  if (M <= 0 || n_active <= 0) return cudaSuccess;
+  picard_residual_kernel<<<dim3(blocks, n_active), 256, 0, s>>>(v, v_prev, M, active_j, partial);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_tube(const float* g0, const float* vfinal, int K, int64_t M, float* tube,
                         cudaStream_t s) {

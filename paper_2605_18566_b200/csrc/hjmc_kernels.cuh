@@ -39,9 +39,27 @@ struct SolveParams {
   float* g0;
   int* err;
   unsigned long long* bad;
+  int skip_stationary;             // HJMC_FLAG_SKIP_STATIONARY
+  unsigned long long* passes;      // Φ passes executed (accounting), nullable
+  // stepwise Picard (kModePass): one pass per (query, active horizon)
+  double* c_state;                 // [K][M] frozen coefficient in, Γ(x, Dv) out
+  const int* active_j;             // [n_active] 1-based horizon indices (device)
+  int n_active;
+  int kiter;                       // Picard iterate index (counter word when crn = 0)
 };
 
-enum : int { kModeSolve = 0, kModeValueGrad = 1 };
+enum : int { kModeSolve = 0, kModeValueGrad = 1, kModePass = 2 };
+
+struct PicardInitParams {
+  const float* x;
+  int64_t M;
+  int K;
+  double* c_state;                 // [K][M] ← Γ(x, Dg(x))
+  float* v_prev;                   // [K][M] ← g(x)  (Algorithm 1: v^(0) = g)
+  GammaParams gp;
+  SystemParams sp;
+  TargetParams tp;
+};
 
 struct EvalParams {
   const float* x;
@@ -58,10 +76,12 @@ struct EvalParams {
 
 using SolveLauncher = cudaError_t (*)(const SolveParams&, int64_t units, cudaStream_t);
 using EvalLauncher = cudaError_t (*)(const EvalParams&, cudaStream_t);
+using PicardInitLauncher = cudaError_t (*)(const PicardInitParams&, cudaStream_t);
 
 struct KernelSet {
   SolveLauncher solve = nullptr;
   EvalLauncher eval_target = nullptr;
+  PicardInitLauncher picard_init = nullptr;
   int threads = 0;
 };
 
@@ -71,6 +91,10 @@ bool lookup_kernels(int target, int n, KernelSet* out);
 cudaError_t launch_tube(const float* g0, const float* vfinal, int K, int64_t M, float* tube,
                         cudaStream_t s);
 cudaError_t launch_hamiltonian(const EvalParams& p, cudaStream_t s);
+// Per active horizon a (grid y) and block b (grid x): partial[a][b] = (Σ (v−v_prev)², Σ v_prev²,
+// max |v−v_prev|) over that block's queries; then v_prev ← v. Deterministic (fixed order).
+cudaError_t launch_picard_residual(const float* v, float* v_prev, int64_t M, const int* active_j,
+                                   int n_active, double* partial, int blocks, cudaStream_t s);
 cudaError_t launch_debug_normals(int n, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
                                  uint32_t count, const RoundKeys& rk, uint32_t tag, int antithetic, float* z,
                                  uint32_t* raw, cudaStream_t s);

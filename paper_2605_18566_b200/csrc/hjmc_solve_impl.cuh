@@ -153,10 +153,14 @@ __device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, flo
 
 // Thread 0's per-iterate epilogue (a9–a10), double precision: v and Dv from the CTA sums,
 // outputs, and the next frozen coefficient Γ(x, Dv) (returned; solve mode only).
+// Exact-stationarity skip (HJMC_FLAG_SKIP_STATIONARY, needs CRN): when Γ returns the same c,
+// the next pass has bit-identical inputs (same samples, same c), hence bit-identical outputs;
+// the remaining iterates are copied instead of recomputed and *done is set.
 template <class Tgt, int NDIM>
 __device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tgt, int64_t m, int j,
                                              int k, uint32_t id, double c, double sigma_d,
-                                             float A, float B, float core_ref, const double* sum) {
+                                             float A, float B, float core_ref, const double* sum,
+                                             bool* done) {
   const double A_d = -c * kLog2e;
   const double Ssum = sum[0];
   // log2 of (1/N) Σ exp(−c g_i): undo the shift B and the fp32 rounding of A
@@ -175,6 +179,19 @@ __device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tg
     atomicMin(P.bad, (unsigned long long)id);
   }
   const bool last = (k == P.Kp - 1);
+  if (P.mode == kModePass) {  // stepwise Picard: [K][M] outputs, state update
+    const size_t o = (size_t)(j - 1) * (size_t)P.M + (size_t)m;
+    if (P.v) P.v[o] = (float)v;
+    if (P.dv)
+      for (int d = 0; d < NDIM; ++d) P.dv[o * NDIM + d] = (float)dv[d];
+    double xd[NDIM];
+    for (int d = 0; d < NDIM; ++d) xd[d] = (double)P.x[m * NDIM + d];
+    const double c_next = gamma_update(P.sp, P.gp, xd, dv);
+    P.c_state[o] = c_next;
+    if (P.c_out) P.c_out[o] = (float)c_next;
+    *done = true;
+    return c_next;
+  }
   if (P.mode != kModeSolve) {
     if (P.v) P.v[m] = (float)v;
     if (P.dv)
@@ -187,7 +204,16 @@ __device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tg
   double xd[NDIM];
   for (int d = 0; d < NDIM; ++d) xd[d] = (double)P.x[m * NDIM + d];
   const double c_next = gamma_update(P.sp, P.gp, xd, dv);           // Γ; dv → p̃
-  if (last) {
+  const bool stationary = P.skip_stationary && P.crn && !last && c_next == c;
+  if (stationary) {
+    for (int kk = k + 1; kk < P.Kp; ++kk) {
+      const size_t h2 = ((size_t)(j - 1) * (size_t)P.Kp + (size_t)kk) * (size_t)P.M + (size_t)m;
+      if (P.vhist) P.vhist[h2] = (float)v;
+      if (P.chist) P.chist[h2] = (float)c;
+    }
+  }
+  *done = last || stationary;
+  if (last || stationary) {
     if (P.vfinal) P.vfinal[(size_t)(j - 1) * (size_t)P.M + (size_t)m] = (float)v;
     if (j == P.K) {
       if (P.v) P.v[m] = (float)v;
@@ -217,6 +243,7 @@ __device__ __noinline__ double unit_prologue(const SolveParams& P, const Tgt& tg
       for (int d = 0; d < NDIM; ++d) P.dv[m * NDIM + d] = (float)p[d];
     return 0.0;
   }
+  if (P.mode == kModePass) return P.c_state[(size_t)(j - 1) * (size_t)P.M + (size_t)m];
   if (P.mode != kModeSolve) return (double)P.c_in[m];
   tgt.dg(xd, p);
   return gamma_update(P.sp, P.gp, xd, p);
@@ -245,6 +272,9 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __g
   if (P.mode == kModeSolve) {
     m = unit / P.K;
     j = (int)(unit % P.K) + 1;
+  } else if (P.mode == kModePass) {
+    m = unit / P.n_active;
+    j = P.active_j[unit % P.n_active];
   } else {
     m = unit;
     j = 1;
@@ -253,7 +283,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __g
 
   // a1: query staging (uniform across the CTA; served from L1 after the first warp)
   const uint32_t id = P.qid ? P.qid[m] : P.qid_base + (uint32_t)m;
-  const double tau = (P.mode == kModeSolve) ? (double)j * P.T / (double)P.K : P.tau_vg;
+  const double tau = (P.mode != kModeValueGrad) ? (double)j * P.T / (double)P.K : P.tau_vg;
   const double sigma_d = sqrt(P.gp.delta_eff * tau);
   const float sigma = (float)sigma_d;
   const float sigma_s = (float)(sigma_d * (double)kBMScale);  // y = x + σ z = x + (σC) ẑ
@@ -273,7 +303,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __g
   if (sm.shift != 0.f) return;  // σ = 0: handled by the prologue (uniform branch)
   __syncthreads();
 
-  const uint32_t jw = (P.mode == kModeSolve) ? (uint32_t)j : P.jtag;
+  const uint32_t jw = (P.mode != kModeValueGrad) ? (uint32_t)j : P.jtag;
   float core_ref;
   {
     float z0[NDIM];
@@ -282,9 +312,12 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __g
     core_ref = tgt.core(xs, 0.f, z0);
   }
   const float lowc = tgt.core_lower(xs, sigma);
+  unsigned passes = 0;  // Φ passes this unit executed (thread 0)
 
   for (int k = 0; k < P.Kp; ++k) {
-    const uint32_t kw = (P.mode == kModeSolve) ? (P.crn ? 0u : (uint32_t)k) : P.ktag;
+    const uint32_t kw = (P.mode == kModeSolve)  ? (P.crn ? 0u : (uint32_t)k)
+                        : (P.mode == kModePass) ? (P.crn ? 0u : (uint32_t)P.kiter)
+                                                : P.ktag;
     const uint32_t w1base = (kw << 8) | (jw << 16);
     const float A = (float)(-c * kLog2e);
     float B = -A * lowc;  // every a_i = A core_i + B ≤ 0: no weight can overflow
@@ -311,12 +344,20 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __g
                                    P.rk, S, Mz);
       cta_reduce<NDIM, NT>(sm, S, Mz);
     }
-    if (threadIdx.x == 0)
-      sm.c_next = pass_epilogue<Tgt, NDIM>(P, tgt, m, j, k, id, c, sigma_d, A, B, core_ref, sm.sum);
+    if (threadIdx.x == 0) {
+      bool done = false;
+      sm.c_next = pass_epilogue<Tgt, NDIM>(P, tgt, m, j, k, id, c, sigma_d, A, B, core_ref, sm.sum,
+                                           &done);
+      sm.shift = done ? 1.f : 0.f;
+      ++passes;
+    }
     __syncthreads();
     c = sm.c_next;
+    const bool done = sm.shift != 0.f;
     __syncthreads();
+    if (done) break;
   }
+  if (threadIdx.x == 0 && P.passes) atomicAdd(P.passes, (unsigned long long)passes);
 }
 
 template <class Tgt, int NDIM, int NT>
@@ -350,6 +391,31 @@ cudaError_t launch_eval_target(const EvalParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Stepwise Picard initialisation (Algorithm 1): v^(0) = g(x), c^(0) = Γ(x, Dg(x)),
+// identical for every horizon.
+template <class Tgt, int NDIM>
+__global__ void picard_init_kernel(const __grid_constant__ PicardInitParams P) {
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= P.M) return;
+  const Tgt tgt(P.tp);
+  double xd[NDIM], p[NDIM];
+  for (int d = 0; d < NDIM; ++d) xd[d] = (double)P.x[m * NDIM + d];
+  const float g = (float)tgt.g_host(xd);
+  tgt.dg(xd, p);
+  const double c0 = gamma_update(P.sp, P.gp, xd, p);
+  for (int j = 0; j < P.K; ++j) {
+    P.c_state[(size_t)j * (size_t)P.M + (size_t)m] = c0;
+    P.v_prev[(size_t)j * (size_t)P.M + (size_t)m] = g;
+  }
+}
+
+template <class Tgt, int NDIM>
+cudaError_t launch_picard_init(const PicardInitParams& p, cudaStream_t s) {
+  if (p.M <= 0) return cudaSuccess;
+  picard_init_kernel<Tgt, NDIM><<<(unsigned)((p.M + 127) / 128), 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
 // One instantiation set per (target, n): the fused solve kernel and the g/Dg evaluator.
 template <template <int> class T, int NDIM>
 KernelSet make_set() {
@@ -357,6 +423,7 @@ KernelSet make_set() {
   KernelSet k;
   k.solve = &launch_solve<T<NDIM>, NDIM, kThreads>;
   k.eval_target = &launch_eval_target<T<NDIM>, NDIM>;
+  k.picard_init = &launch_picard_init<T<NDIM>, NDIM>;
   k.threads = kThreads;
   return k;
 }

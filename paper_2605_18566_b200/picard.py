@@ -1,0 +1,117 @@
+"""Algorithm 1 with its convergence test, driven through the C-ABI's stepwise Picard calls,
+plus Theorem 2's contraction diagnostics.
+
+Algorithm 1 stops when ε = ‖v^(k+1) − v^(k)‖/‖v^(k)‖ < tol (step 5; relative L2
+over the slice's queries, R11), per horizon j. The norms are slice-wide — with queries sharded
+over GPUs the per-rank partial sums (hjmc_picard_pass) are all-reduced before the decision, so
+every rank takes the same decision. Every Φ pass and Γ update runs in the CUDA kernels; this
+module only sums six numbers per horizon and applies the stopping rule.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+
+def contraction_constant(G: float, c_min: float, L_D: float, delta: float, L_H: float,
+                         m0: float, H_star: float, P_star: float) -> float:
+    """q of Assumption 1 item 5 (Eq. contraction_const; R18 uses 2G/c_min):
+    q = (2G/c_min)·(2 L_D/δ)·(L_H/m0² + 2 H* P*/m0⁴)."""
+    return (2.0 * G / c_min) * (2.0 * L_D / delta) * (L_H / m0**2 + 2.0 * H_star * P_star / m0**4)
+
+
+@dataclass
+class ContractionReport:
+    """Theorem 2 diagnostics from the sup-norm Picard differences d_k = ‖v^(k+1) −
+    v^(k)‖∞: empirical ratios q̂_k = d_k / d_{k−1}; with a theoretical q < 1, the geometric
+    bound d_k ≤ q^k d_0 (Eq. gamma-lip-cauchy) and the a-posteriori error bound
+    ‖v^(k) − v*‖∞ ≤ q/(1−q)·‖v^(k) − v^(k−1)‖∞ (Eq. aposteriori-error)."""
+
+    d_sup: np.ndarray
+    q_hat: np.ndarray
+    q_theory: float | None
+    aposteriori: np.ndarray | None
+    certified: bool
+
+    @classmethod
+    def from_differences(cls, d_sup, q_theory: float | None = None) -> "ContractionReport":
+        d = np.asarray(d_sup, dtype=np.float64)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            q_hat = d[1:] / d[:-1] if d.size >= 2 else np.zeros(0)
+        apost = None
+        certified = q_theory is not None and 0.0 <= q_theory < 1.0
+        if certified:
+            apost = q_theory / (1.0 - q_theory) * d   # bound on ‖v^(k+1) − v*‖∞ from d_k
+        return cls(d, q_hat, q_theory, apost, certified)
+
+
+def solve_adaptive(solver, x, tol: float, max_iter: int, qid_base: int = 0, qid=None,
+                   drift=None, allreduce=None, want_dv: bool = True):
+    """Run Algorithm 1 per horizon until ε_j(k) < tol or max_iter passes.
+
+    allreduce(partials[K][3] float64) -> partials: combine shards (sum cols 0–1, max col 2);
+    None for a single process. Returns a dict: v, dv, c [K][M](…) device tensors of each
+    horizon's final iterate, iters [K], eps [K][max_iter], d_sup [K][max_iter] (NaN past the
+    stop), tube [M] = min(g, min_j v_j), converged [K]."""
+    t = solver.torch
+    cfg = solver.cfg
+    x = solver._as_dev(x)
+    M, K, n = x.shape[0], cfg.K, cfg.n
+    q = solver._as_dev(qid, t.int32) if qid is not None else None
+    b = solver._as_dev(drift) if drift is not None else None
+    L = solver.L
+    stream = solver._stream()
+    solver._check(L.hjmc_picard_begin(solver.h, C.c_void_p(x.data_ptr()),
+                                      C.c_void_p(q.data_ptr()) if q is not None else None,
+                                      qid_base, M, C.c_void_p(b.data_ptr()) if b is not None else None,
+                                      stream))
+    v = t.empty((K, M), device=solver.device)
+    dv = t.empty((K, M, n), device=solver.device) if want_dv else None
+    c = t.empty((K, M), device=solver.device)
+    active = np.ones(K, dtype=np.uint8)
+    iters = np.zeros(K, dtype=np.int64)
+    eps = np.full((K, max_iter), np.nan)
+    dsup = np.full((K, max_iter), np.nan)
+    part = np.zeros((K, 3), dtype=np.float64)
+    for k in range(max_iter):
+        if not active.any():
+            break
+        solver._check(L.hjmc_picard_pass(
+            solver.h, k, active.ctypes.data_as(C.c_void_p), C.c_void_p(v.data_ptr()),
+            C.c_void_p(dv.data_ptr()) if dv is not None else None, C.c_void_p(c.data_ptr()),
+            part.ctypes.data_as(C.c_void_p), stream))
+        tot = allreduce(part.copy()) if allreduce is not None else part
+        for j in np.flatnonzero(active):
+            iters[j] = k + 1
+            eps[j, k] = np.sqrt(tot[j, 0] / max(tot[j, 1], 1e-300))
+            dsup[j, k] = tot[j, 2]
+            if eps[j, k] < tol:
+                active[j] = 0
+    g, _ = solver.eval_target(x)
+    tube = t.minimum(g, v.min(dim=0).values)
+    return {"v": v, "dv": dv, "c": c, "iters": iters, "eps": eps, "d_sup": dsup, "tube": tube,
+            "converged": ~active.astype(bool), "g0": g}
+
+
+def torch_allreduce(group=None):
+    """An allreduce for solve_adaptive over torch.distributed (NCCL or gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    def f(part):
+        s = torch.from_numpy(np.ascontiguousarray(part[:, :2]))
+        m = torch.from_numpy(np.ascontiguousarray(part[:, 2]))
+        if dist.get_backend(group) == "nccl":
+            s, m = s.cuda(), m.cuda()
+        dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+        out = part.copy()
+        out[:, :2] = s.cpu().numpy()
+        out[:, 2] = m.cpu().numpy()
+        return out
+
+    return f

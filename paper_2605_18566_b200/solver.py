@@ -32,6 +32,7 @@ class SolverConfig:
     tag: int = 0
     device: int = 0
     sync_check: bool = False
+    skip_stationary: bool = False
     system: str = "quadratic"
     sys_params: tuple = ()
     target: str = "quad_bowl"
@@ -53,7 +54,8 @@ class SolverConfig:
         c.visc = _lib.VISC[self.visc]
         c.crn, c.antithetic = int(self.crn), int(self.antithetic)
         c.m0, c.c_min, c.c_max, c.tag, c.device = self.m0, self.c_min, self.c_max, self.tag, self.device
-        c.flags = _lib.FLAG_SYNC_CHECK if self.sync_check else 0
+        c.flags = (_lib.FLAG_SYNC_CHECK if self.sync_check else 0) | (
+            _lib.FLAG_SKIP_STATIONARY if self.skip_stationary else 0)
         return c
 
 
@@ -205,6 +207,12 @@ class Solver:
     def check(self):
         """Synchronise and raise HjmcError(ENUMERIC) on a recorded numerical failure."""
         self._check(self.L.hjmc_check(self.h, self._stream()))
+
+    def pass_count(self) -> int:
+        """Φ passes executed since the previous call (synchronises)."""
+        v = C.c_uint64()
+        self._check(self.L.hjmc_pass_count(self.h, self._stream(), C.byref(v)))
+        return int(v.value)
 
     def last_bad_query(self) -> int:
         return int(self.L.hjmc_last_bad_query(self.h))

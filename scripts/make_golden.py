@@ -1,0 +1,57 @@
+"""Write tests/golden/<config>_sample.npz: oracle (only) results at BASELINE.json's FULL sizes
+for a deterministic sample of each config's global query ids. The GPU parity test replays the
+same global ids through the CUDA path (results depend only on global ids, so this equals the
+full launch). Sample = an even spread, the queries nearest the target boundary band
+(|g(x)| ≤ σ_K·8.16, where the BRT boundary lies), and queries whose c^(0) is unclamped (R8).
+Usage: python scripts/make_golden.py c3 c4 c5 [--threads T]"""
+import math
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle as O  # noqa: E402
+from paper_2605_18566_b200 import inputs as I  # noqa: E402
+
+COUNTS = {3: (12, 6, 6), 4: (6, 3, 3), 5: (4, 2, 2)}
+
+
+def sample_ids(p, P, x, n_spread, n_band, n_int):
+    M = x.shape[0]
+    spread = I.subsample_ids(M, n_spread)
+    stride = max(1, M // 4000)                       # scan a thinned grid for the picks
+    cand = np.arange(0, M, stride)
+    g = np.array([O.g(P, x[m].astype(np.float64)) for m in cand])
+    band = math.sqrt(P.delta_eff * p.T) * 8.16
+    near = cand[np.argsort(np.abs(g))][:n_band]
+    c0 = np.array([O.gamma(P, x[m].astype(np.float64), O.dg(P, x[m].astype(np.float64))) for m in cand])
+    inter = cand[(c0 > p.c_min * 1.01) & (c0 < p.c_max * 0.99)]
+    inter = inter[np.linspace(0, len(inter) - 1, min(n_int, len(inter))).round().astype(int)] if len(inter) else inter
+    return np.unique(np.concatenate([spread, near, inter])).astype(np.int64)
+
+
+def main():
+    which = [int(a.lstrip("c")) for a in sys.argv[1:] if a.startswith("c")] or [3, 4, 5]
+    threads = int(sys.argv[sys.argv.index("--threads") + 1]) if "--threads" in sys.argv else 0
+    for idx in which:
+        p = I.BY_INDEX[idx]
+        P = O.Problem.from_preset(p)
+        x = I.queries(p)
+        ids = sample_ids(p, P, x, *COUNTS[idx])
+        t0 = time.time()
+        r = O.solve_slice(P, x[ids], qids=ids.astype(np.uint32), nthreads=threads)
+        dt = time.time() - t0
+        assert r["status"] == 0
+        path = os.path.join(ROOT, "tests", "golden", f"{p.name}_sample.npz")
+        np.savez_compressed(path, ids=ids, x=x[ids], v=r["v"], dv=r["dv"], c=r["c"], tube=r["tube"],
+                            vhist=r["vhist"], chist=r["chist"], dvhist=r["dvhist"], g0=r["g0"],
+                            source=np.array("scripts/make_golden.py -> oracle.solve_slice (double); "
+                                            f"preset {p.name}; {dt:.0f} s on {O.max_threads()} threads"))
+        print(f"{p.name}: {len(ids)} queries in {dt:.0f} s -> {path}", flush=True)
+
+
+if __name__ == "__main__":
+    main()

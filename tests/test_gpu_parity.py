@@ -262,3 +262,64 @@ def test_c2_full_size_sampled(O):
     assert_dv(out["dv"][ids], ref["dv"])
     assert_v(out["tube"][ids], ref["tube"], "tube")
     np.testing.assert_allclose(out["g0"][ids], ref["g0"], rtol=1e-6, atol=1e-6)
+
+
+def test_skip_stationary_is_bit_identical():
+    """HJMC_FLAG_SKIP_STATIONARY copies iterates whose inputs are bit-identical (c unchanged
+    under CRN): every output must equal the full computation exactly, with fewer passes."""
+    kw = dict(N=3000, K=3, Kp=5)
+    base = Solver(SolverConfig.from_preset(I.C2, **kw))
+    fast = Solver(SolverConfig.from_preset(I.C2, skip_stationary=True, **kw))
+    x = I.queries(I.C2)[::13]
+    M = x.shape[0]
+    a = base.solve_slice(x)
+    na = base.pass_count()
+    b = fast.solve_slice(x)
+    nb = fast.pass_count()
+    for k in a:
+        assert torch.equal(a[k], b[k]), k
+    assert na == M * 3 * 5
+    assert nb < na
+    # without CRN nothing may be skipped
+    nocrn = Solver(SolverConfig.from_preset(I.C2, skip_stationary=True, crn=False, **kw))
+    nocrn.solve_slice(x)
+    assert nocrn.pass_count() == M * 3 * 5
+
+
+def test_picard_stepwise_equals_fused_solve():
+    """hjmc_picard_pass with every horizon active reproduces hjmc_solve_slice's iterates
+    bit for bit (same counters, same kernel body)."""
+    from paper_2605_18566_b200.picard import solve_adaptive
+
+    p = I.C2.with_(N=2000, K=3, Kp=4)
+    s = Solver(SolverConfig.from_preset(p, crn=False))
+    x = I.queries(p)[::97]
+    fused = s.solve_slice(x, qid_base=5)
+    r = solve_adaptive(s, x, tol=0.0, max_iter=4, qid_base=5)
+    assert list(r["iters"]) == [4, 4, 4]
+    assert torch.equal(r["v"], fused["vhist"][:, -1])
+    assert torch.equal(r["c"][-1], fused["c"])
+    assert torch.equal(r["dv"][-1], fused["dv"])
+    assert torch.equal(r["tube"], fused["tube"])
+
+
+def test_picard_adaptive_vs_oracle(O):
+    """Algorithm 1 with its stopping test: GPU driver vs the oracle's, same iteration counts,
+    residual histories and final values (C2 physics, small N)."""
+    from paper_2605_18566_b200.picard import solve_adaptive
+
+    p = I.C2.with_(N=3000, K=3)
+    x = I.queries(p)[::53]
+    P = O.Problem.from_preset(p, crn=False)
+    ref = O.picard_adaptive(P, x, 0.0, 5)
+    s = Solver(SolverConfig.from_preset(p, crn=False))
+    r = solve_adaptive(s, x, tol=0.0, max_iter=5)
+    np.testing.assert_allclose(r["eps"], ref["eps"], rtol=0.05, atol=1e-7)
+    e = np.sort(ref["eps"][np.isfinite(ref["eps"]) & (ref["eps"] > 0)])
+    gap = int(np.argmax(e[1:] / e[:-1]))                # threshold far from every eps value
+    tol = float(np.sqrt(e[gap] * e[gap + 1]))
+    ref_t = O.picard_adaptive(P, x, tol, 5)
+    r_t = solve_adaptive(s, x, tol=tol, max_iter=5)
+    assert list(r_t["iters"]) == list(ref_t["iters"])
+    for j in range(3):
+        assert_v(r_t["v"][j].cpu().numpy(), ref_t["v"][j], f"v[{j}]")
