@@ -19,8 +19,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "hjmc_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
 
-SYSTEMS = {"quadratic": 0, "dubins_rel": 1, "rocket6": 2, "dubins_pairs": 3}
-TARGETS = {"quad_bowl": 0, "disk": 1, "rel_disk6": 2, "pair_union": 3, "linear": 4, "const": 5}
+SYSTEMS = {"quadratic": 0, "dubins_rel": 1, "rocket6": 2, "dubins_pairs": 3, "rocket3": 4,
+           "double_integrator": 5, "multiagent": 6}
+TARGETS = {"quad_bowl": 0, "disk": 1, "rel_disk6": 2, "pair_union": 3, "linear": 4, "const": 5,
+           "pursuit_min": 6}
+AVOIDS = {"none": 0, "disk": 1}
 
 
 def build(force: bool = False) -> str:
@@ -39,6 +42,7 @@ class _Problem(C.Structure):
         ("m0", C.c_double), ("c_min", C.c_double), ("c_max", C.c_double), ("tag", C.c_uint32),
         ("system", C.c_int32), ("n_sys_params", C.c_int32), ("sys_params", C.c_double * 8),
         ("target", C.c_int32), ("n_tgt_params", C.c_int32), ("tgt_params", C.c_double * 72),
+        ("avoid", C.c_int32), ("avoid_params", C.c_double * 3),
     ]
 
 
@@ -57,6 +61,8 @@ def lib():
         L.orc_target_g.argtypes = [pp, dp]
         L.orc_target_g.restype = C.c_double
         L.orc_target_dg.argtypes = [pp, dp, dp]
+        L.orc_avoid_l.argtypes = [pp, dp]
+        L.orc_avoid_l.restype = C.c_double
         L.orc_hamiltonian.argtypes = [pp, dp, dp]
         L.orc_hamiltonian.restype = C.c_double
         L.orc_gamma.argtypes = [pp, dp, dp]
@@ -100,13 +106,16 @@ class Problem:
     sys_params: tuple = ()
     target: str = "quad_bowl"
     tgt_params: tuple = ()
+    avoid: str = "none"
+    avoid_params: tuple = ()
 
     @classmethod
     def from_preset(cls, p, **kw):
         d = dict(n=p.n, delta=p.delta, T=p.T, K=p.K, Kp=p.Kp, N=p.N, seed=p.seed, visc=p.visc,
                  crn=p.crn, antithetic=p.antithetic, m0=p.m0, c_min=p.c_min, c_max=p.c_max,
                  tag=p.tag, system=p.system, sys_params=tuple(p.sys_params), target=p.target,
-                 tgt_params=tuple(p.tgt_params))
+                 tgt_params=tuple(p.tgt_params), avoid=getattr(p, "avoid", "none"),
+                 avoid_params=tuple(getattr(p, "avoid_params", ())))
         d.update(kw)
         return cls(**d)
 
@@ -125,6 +134,9 @@ class Problem:
         s.n_tgt_params = len(self.tgt_params)
         for i, v in enumerate(self.tgt_params):
             s.tgt_params[i] = v
+        s.avoid = AVOIDS[self.avoid]
+        for i, v in enumerate(self.avoid_params):
+            s.avoid_params[i] = v
         return s
 
     @property
@@ -164,6 +176,11 @@ def dg(P: Problem, x) -> np.ndarray:
     o = np.zeros(P.n)
     lib().orc_target_dg(C.byref(P.struct()), _dp(x), _dp(o))
     return o
+
+
+def avoid_l(P: Problem, x) -> float:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    return lib().orc_avoid_l(C.byref(P.struct()), _dp(x))
 
 
 def hamiltonian(P: Problem, x, p) -> float:

@@ -111,8 +111,29 @@ double orc_target_g(const orc_problem* P, const double* y) {
     }
     case ORC_TGT_CONST:
       return tparam(P, 0, 0.0);
+    case ORC_TGT_PURSUIT_MIN: { /* min over pursuers i of ||pos_i - pos_evader|| - r */
+      int A = n / 3;
+      const double* e = y + 3 * (A - 1);
+      double best = INFINITY;
+      for (int i = 0; i < A - 1; ++i) {
+        double dx = y[3 * i] - e[0], dy = y[3 * i + 1] - e[1];
+        double d = sqrt(dx * dx + dy * dy);
+        if (d < best) best = d;
+      }
+      return best - tparam(P, 0, 1.5);
+    }
   }
   return NAN;
+}
+
+/* BRAT avoid function l(x): positive inside the obstacle; the tube is
+ * clamped to max(tube, l(x)) so states inside the avoid set are excluded from the BRAT. */
+double orc_avoid_l(const orc_problem* P, const double* x) {
+  if (P->avoid == ORC_AVOID_DISK) {
+    double dx = x[0] - P->avoid_params[0], dy = x[1] - P->avoid_params[1];
+    return P->avoid_params[2] - sqrt(dx * dx + dy * dy);
+  }
+  return -INFINITY;
 }
 
 /* Analytic Dg for c^(0) (R7: e1 at the singular point of a distance). */
@@ -154,6 +175,24 @@ void orc_target_dg(const orc_problem* P, const double* x, double* dg) {
       return;
     case ORC_TGT_CONST:
       return;
+    case ORC_TGT_PURSUIT_MIN: {
+      int A = n / 3, arg = 0;
+      const double* e = x + 3 * (A - 1);
+      double best = INFINITY;
+      for (int i = 0; i < A - 1; ++i) {
+        double dx = x[3 * i] - e[0], dy = x[3 * i + 1] - e[1];
+        double d = sqrt(dx * dx + dy * dy);
+        if (d < best) { best = d; arg = i; }   /* first minimiser on ties */
+      }
+      if (best > 0.0) {
+        double dx = (x[3 * arg] - e[0]) / best, dy = (x[3 * arg + 1] - e[1]) / best;
+        dg[3 * arg] = dx; dg[3 * arg + 1] = dy;
+        dg[3 * (A - 1)] = -dx; dg[3 * (A - 1) + 1] = -dy;
+      } else {
+        dg[0] = 1.0;
+      }
+      return;
+    }
   }
 }
 
@@ -189,6 +228,25 @@ double orc_hamiltonian(const orc_problem* P, const double* x, const double* p) {
         h += a * (pv[0] * cos(xv[2]) + pv[1] * sin(xv[2])) - grav * pv[1];
       }
       h += -fabs(p[2]) + fabs(p[5]) + dmax * sqrt(p[3] * p[3] + p[4] * p[4]);
+      return h;
+    }
+    case ORC_SYS_ROCKET3: { /* Eq. rocket_ham_simplified, verbatim (R14) */
+      double a = sparam(P, 0, 64.0), grav = sparam(P, 1, 32.0);
+      return -(a * p[0] * cos(x[2]) + p[1] * (a + a * sin(x[2]) - grav) -
+               fabs(p[0] * x[0] + p[2]) - fabs(p[1] * x[0] - p[2]));
+    }
+    case ORC_SYS_DOUBLE_INTEGRATOR: /* Eq. dint_ham P:1300–1303 with u = -sign(p2) */
+      return p[0] * x[1] - fabs(p[1]);
+    case ORC_SYS_MULTIAGENT: { /* agents (x, y, theta), speed a_i, |u_i| <= 1; last =
+                                  evader (maximises), others pursuers (minimise) */
+      int A = n / 3;
+      double ap = sparam(P, 0, 1.0), ae = sparam(P, 1, 1.0);
+      double h = 0.0;
+      for (int i = 0; i < A; ++i) {
+        double a = (i == A - 1) ? ae : ap;
+        h += a * (p[3 * i] * cos(x[3 * i + 2]) + p[3 * i + 1] * sin(x[3 * i + 2]));
+        h += (i == A - 1) ? fabs(p[3 * i + 2]) : -fabs(p[3 * i + 2]);
+      }
       return h;
     }
     case ORC_SYS_DUBINS_PAIRS: { /* R16: sum of independent relative Dubins pairs */
@@ -372,6 +430,8 @@ int orc_solve_slice(const orc_problem* P, const float* x, const float* drift, co
       double vj = vfinal[(size_t)j * (size_t)M + (size_t)m];
       if (vj < t) t = vj;
     }
+    double l = orc_avoid_l(P, xm);                   /* BRAT clamp: max(tube, l) */
+    if (l > t) t = l;
     if (tube) tube[m] = t;
   }
   free(vfinal);

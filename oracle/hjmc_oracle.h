@@ -28,9 +28,11 @@ extern "C" {
 #endif
 
 /* Oracle-side identifiers (the tests map them to the library's). */
-enum { ORC_SYS_QUADRATIC = 0, ORC_SYS_DUBINS_REL = 1, ORC_SYS_ROCKET6 = 2, ORC_SYS_DUBINS_PAIRS = 3 };
+enum { ORC_SYS_QUADRATIC = 0, ORC_SYS_DUBINS_REL = 1, ORC_SYS_ROCKET6 = 2, ORC_SYS_DUBINS_PAIRS = 3,
+       ORC_SYS_ROCKET3 = 4, ORC_SYS_DOUBLE_INTEGRATOR = 5, ORC_SYS_MULTIAGENT = 6 };
 enum { ORC_TGT_QUAD_BOWL = 0, ORC_TGT_DISK = 1, ORC_TGT_REL_DISK6 = 2, ORC_TGT_PAIR_UNION = 3,
-       ORC_TGT_LINEAR = 4, ORC_TGT_CONST = 5 };
+       ORC_TGT_LINEAR = 4, ORC_TGT_CONST = 5, ORC_TGT_PURSUIT_MIN = 6 };
+enum { ORC_AVOID_NONE = 0, ORC_AVOID_DISK = 1 };
 
 #define ORC_MAX_N 64
 #define ORC_MAX_PARAMS 72
@@ -56,12 +58,15 @@ typedef struct orc_problem {
   int32_t target;
   int32_t n_tgt_params;
   double tgt_params[ORC_MAX_PARAMS];
+  int32_t avoid;            /* BRAT obstacle: ORC_AVOID_* */
+  double avoid_params[3];   /* disk: centre (x0, x1) and radius */
 } orc_problem;
 
 void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 void orc_sample_normals(const orc_problem* P, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i,
                         double* z, uint32_t* raw);
 double orc_target_g(const orc_problem* P, const double* y);
+double orc_avoid_l(const orc_problem* P, const double* x);
 void orc_target_dg(const orc_problem* P, const double* x, double* dg);
 double orc_hamiltonian(const orc_problem* P, const double* x, const double* p);
 double orc_gamma(const orc_problem* P, const double* x, const double* p);

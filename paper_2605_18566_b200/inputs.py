@@ -41,6 +41,8 @@ class Preset:
     c_max: float = 20.0
     seed: int = SEED_BASE
     tag: int = 0
+    avoid: str = "none"          # BRAT obstacle: "none" | "disk"
+    avoid_params: tuple = ()     # disk: (centre x0, centre x1, radius)
     # slice layout
     grid_axes: tuple = (0, 1)    # which state coordinates vary over the 2-D grid
     grid_lo: float = -1.0
@@ -133,7 +135,40 @@ PAPER_DUBINS = Preset(
     grid_lo=-5.0, grid_hi=5.0, grid_pts=40, fixed=(0.0, 0.0, 0.0), seed=SEED_BASE + 5,
 )
 
-PRESETS = {p.name: p for p in (C1, C2, C3, C4, C5, PAPER_DUBINS)}
+# The paper's own systems, context presets:
+# 3-D rockets, Eq. rocket_ham_simplified, a = 64, g = 32, capture r = 1.5
+# (P:1385), δ = 0.08 and N = 14,000, slice θ = 0 over a window of (−100, 100]².
+PAPER_ROCKETS = Preset(
+    name="paper_rockets3_40x40", n=3, delta=0.08, T=1.0, K=1, Kp=12, N=14000,
+    system="rocket3", target="disk", sys_params=(64.0, 32.0), tgt_params=(1.5,),
+    grid_lo=-10.0, grid_hi=10.0, grid_pts=40, fixed=(0.0, 0.0, 0.0), seed=SEED_BASE + 6,
+)
+# Double integrator (Table 4: N = 8,000, δ = 0.08, 15 iterations), target ball of
+# radius 0.1 around the origin, t-slices as horizons-to-go.
+PAPER_DOUBLE_INTEGRATOR = Preset(
+    name="paper_double_integrator", n=2, delta=0.08, T=0.8, K=4, Kp=15, N=8000,
+    system="double_integrator", target="disk", tgt_params=(0.1,),
+    grid_lo=-1.0, grid_hi=1.0, grid_pts=40, seed=SEED_BASE + 7,
+)
+# 45-D game: 14 pursuers + 1 evader (x, y, θ), capture r = 1.5; regime 2 (all speeds
+# 1); slice: the evader's (x, y) free on [−20, 20]², pursuer i at (15 cos φ_i, 15 sin φ_i), θ = 0.
+def _ring(A, radius):
+    s = [0.0] * (3 * A)
+    for i in range(A - 1):
+        ph = 2 * math.pi * i / (A - 1)
+        s[3 * i], s[3 * i + 1] = radius * math.cos(ph), radius * math.sin(ph)
+    return tuple(s)
+
+
+PAPER_MULTIAGENT45 = Preset(
+    name="paper_multiagent45", n=45, delta=0.08, T=1.0, K=1, Kp=15, N=1 << 14,
+    system="multiagent", target="pursuit_min", sys_params=(1.0, 1.0), tgt_params=(1.5,),
+    grid_axes=(42, 43), grid_lo=-20.0, grid_hi=20.0, grid_pts=32, fixed=_ring(15, 15.0),
+    seed=SEED_BASE + 8,
+)
+
+PRESETS = {p.name: p for p in (C1, C2, C3, C4, C5, PAPER_DUBINS, PAPER_ROCKETS,
+                                PAPER_DOUBLE_INTEGRATOR, PAPER_MULTIAGENT45)}
 BY_INDEX = {1: C1, 2: C2, 3: C3, 4: C4, 5: C5}
 
 

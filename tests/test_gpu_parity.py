@@ -323,3 +323,31 @@ def test_picard_adaptive_vs_oracle(O):
     assert list(r_t["iters"]) == list(ref_t["iters"])
     for j in range(3):
         assert_v(r_t["v"][j].cpu().numpy(), ref_t["v"][j], f"v[{j}]")
+
+
+@pytest.mark.parametrize("idx", [3, 4, 5])
+def test_full_size_configs_golden(O, idx):
+    """BASELINE configs 3–5 at FULL size (N = 2^18 / 2^20, all horizons and Picard iterates) on
+    the sampled global query ids stored by scripts/make_golden.py (oracle-only values). The
+    GPU replays the same global ids; results depend only on them, so this equals the full
+    slice launch for those queries."""
+    import os
+
+    p = I.BY_INDEX[idx]
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", f"{p.name}_sample.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    d = np.load(path)
+    ids = d["ids"]
+    s = Solver(SolverConfig.from_preset(p))
+    out = {k: t.cpu().numpy() for k, t in s.solve_slice(d["x"], qid=ids.astype(np.int32)).items()}
+    s.check()
+    ref = {k: d[k] for k in ("v", "dv", "c", "tube", "vhist", "chist", "dvhist", "g0")}
+    for j in range(p.K):
+        for k in range(p.Kp):
+            assert_v(out["vhist"][j, k], ref["vhist"][j, k], f"vhist[{j},{k}]")
+    assert_c_history(O, O.Problem.from_preset(p), d["x"], out["chist"], ref)
+    assert_v(out["v"], ref["v"])
+    assert_dv(out["dv"], ref["dv"])
+    assert_v(out["tube"], ref["tube"], "tube")
+    np.testing.assert_allclose(out["g0"], ref["g0"], rtol=1e-6, atol=1e-6)

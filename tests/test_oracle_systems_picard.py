@@ -204,3 +204,102 @@ def test_corollary1_sample_size():
     alpha, beta = math.exp(-c * gmax), math.exp(-c * gmin)
     N = (beta - alpha) ** 2 / (2 * alpha**2 * (1 - math.exp(-c * eps)) ** 2) * math.log(2 / alpha)
     assert abs(N - 276.008) < 1e-3
+
+
+# ---- the paper's own systems -------------------------------------
+def test_rocket3_spec_cases(oracle_mod):
+    """Eq. rocket_ham_simplified: S:113 H((0,0,0),(1,0,0)) = −64; S:213 Γ clamps
+    c_raw = 2·(−64)/(0.08·1) = −1600 to c_min."""
+    O = oracle_mod
+    P = O.Problem(n=3, delta=0.08, system="rocket3", sys_params=(64.0, 32.0))
+    assert O.hamiltonian(P, (0, 0, 0), (1, 0, 0)) == -64.0
+    assert O.hamiltonian(P, (3, -1, 0.4), (0, 0, 0)) == 0.0
+    assert O.gamma(P, np.zeros(3), np.array([1.0, 0, 0])) == P.c_min
+    # p2 term: −p2 (a + a sin θ − g) at θ = π/2, x = 0: −(64 + 64 − 32) = −96
+    assert abs(O.hamiltonian(P, (0, 0, math.pi / 2), (0, 1, 0)) - (-96.0)) < 1e-12
+    # |p1 x + p3| and |p2 x − p3| enter with + sign after the outer minus
+    assert abs(O.hamiltonian(P, (2.0, 0, math.pi), (0, 0, 1)) - 2.0) < 1e-12
+
+
+def test_double_integrator_spec_cases(oracle_mod):
+    """Eq. dint_ham with u = −sign(p2) (P:1300–1307): S:130–131."""
+    O = oracle_mod
+    P = O.Problem(n=2, system="double_integrator")
+    assert O.hamiltonian(P, (0, 2), (1, 0)) == 2.0
+    assert O.hamiltonian(P, (5, -3), (0, 1)) == -1.0
+    assert O.hamiltonian(P, (1, 1), (0, 0)) == 0.0
+
+
+def test_multiagent_cases(oracle_mod):
+    """P:389–401 dynamics, S:151's Hamiltonian and S:141–143's target cases."""
+    O = oracle_mod
+    P = O.Problem(n=9, system="multiagent", sys_params=(1.0, 2.0), target="pursuit_min",
+                  tgt_params=(1.5,))
+    e = np.eye(9)
+    x = np.zeros(9)
+    assert O.hamiltonian(P, x, np.zeros(9)) == 0.0
+    assert O.hamiltonian(P, x, e[0]) == 1.0          # pursuer speed 1, heading 0
+    assert O.hamiltonian(P, x, e[6]) == 2.0          # evader speed 2
+    assert O.hamiltonian(P, x, e[2]) == -1.0         # pursuer turn −|p_θ|
+    assert O.hamiltonian(P, x, e[8]) == 1.0          # evader turn +|p_θ|
+    assert O.g(P, np.zeros(9)) == -1.5               # all at the origin
+    y = np.zeros(9)
+    y[6] = 10.0                                       # evader at (10, 0), pursuers at origin and far
+    y[3] = 100.0
+    assert O.g(P, y) == 8.5
+    rng = np.random.default_rng(0)
+    for _ in range(10):
+        xx, p = rng.normal(size=9) * 3, rng.normal(size=9)
+        assert abs(O.hamiltonian(P, xx, 3 * p) - 3 * O.hamiltonian(P, xx, p)) < 1e-9
+
+
+def test_pursuit_min_quadrature(oracle_mod):
+    """2 agents: g depends on pos_0 − pos_1 ~ N(Δ, 2σ² I2), so 2-D Gauss–Hermite pins Φ."""
+    from numpy.polynomial.hermite_e import hermegauss
+
+    O = oracle_mod
+    c, tau, r = 2.0, 4.0, 1.5
+    P = O.Problem(n=6, delta=0.01, N=1 << 16, system="multiagent", target="pursuit_min",
+                  tgt_params=(r,))
+    s = math.sqrt(0.01 * tau)
+    x = np.array([1.3, 0.4, 0.2, -0.6, 0.9, 0.0])
+    dx, dy = x[0] - x[3], x[1] - x[4]
+    t, w = hermegauss(160)
+    w = w / math.sqrt(2 * math.pi)
+    Z1, Z2 = np.meshgrid(t, t, indexing="ij")
+    W = np.outer(w, w) * np.exp(-c * (np.hypot(dx + math.sqrt(2) * s * Z1, dy + math.sqrt(2) * s * Z2) - r))
+    v_q = -math.log(W.sum()) / c
+    v, dv, diag, se = O.phi(P, x, c, tau, qid=2)
+    assert abs(v - v_q) < 4.5 * diag[3]
+
+
+@pytest.mark.parametrize("target,n,params", [("pursuit_min", 9, (1.5,))])
+def test_pursuit_min_gradient_fd(oracle_mod, target, n, params):
+    O = oracle_mod
+    P = O.Problem(n=n, target=target, tgt_params=params)
+    rng = np.random.default_rng(7)
+    for _ in range(5):
+        x = rng.uniform(-3, 3, n)
+        h = 1e-6
+        fd = np.array([(O.g(P, x + h * e) - O.g(P, x - h * e)) / (2 * h) for e in np.eye(n)])
+        np.testing.assert_allclose(O.dg(P, x), fd, atol=1e-7)
+
+
+def test_brat_clamp(oracle_mod):
+    """HJI-RCBRAT-Visc realised as tube ← max(tube, ℓ(x)): no obstacle →
+    BRT unchanged; ℓ > g everywhere → tube = ℓ; always tube ≥ ℓ."""
+    O = oracle_mod
+    base = dict(n=2, delta=0.08, T=0.8, K=2, Kp=2, N=600, system="double_integrator",
+                target="disk", tgt_params=(0.1,))
+    x = np.random.default_rng(1).uniform(-1, 1, (30, 2)).astype(np.float32)
+    brt = O.solve_slice(O.Problem(**base), x)
+    none = O.solve_slice(O.Problem(**base, avoid="none"), x)
+    np.testing.assert_array_equal(brt["tube"], none["tube"])
+    P = O.Problem(**base, avoid="disk", avoid_params=(0.2, -0.1, 0.35))
+    brat = O.solve_slice(P, x)
+    ell = np.array([O.avoid_l(P, xm.astype(np.float64)) for xm in x])
+    np.testing.assert_array_equal(brat["tube"], np.maximum(brt["tube"], ell))
+    assert np.all(brat["tube"][ell > 0] > 0)          # obstacle interior excluded from the BRAT
+    huge = O.Problem(**base, avoid="disk", avoid_params=(0.0, 0.0, 50.0))
+    np.testing.assert_array_equal(O.solve_slice(huge, x)["tube"],
+                                  [O.avoid_l(huge, xm.astype(np.float64)) for xm in x])
