@@ -70,6 +70,13 @@
  *            + d_max · ‖(p_xE, p_zE)‖
  *  HJMC_SYS_DUBINS_PAIRS  n = 3K   params {v_p, v_e, w} = {5, 5, 1}              (R16)
  *        H = Σ_{q<K} H_DUBINS_REL(x[3q..3q+2], p[3q..3q+2])
+ *  HJMC_SYS_ROCKET3       n = 3    params {a, g_grav} = {64, 32}        (R14)
+ *        state (x, z, θ);  H = −[ a p1 cos θ + p2 (a + a sin θ − g) − |p1 x + p3| − |p2 x − p3| ]
+ *  HJMC_SYS_DOUBLE_INTEGRATOR n = 2  no params
+ *        H = p1 x2 − |p2|   (ẋ1 = x2, ẋ2 = u, |u| ≤ 1, u = −sign(p2))
+ *  HJMC_SYS_MULTIAGENT    n = 3A   params {a_pursuer, a_evader} = {1, 1}
+ *        agents (x_i, y_i, θ_i), ẋ = a cos θ, ẏ = a sin θ, θ̇ = u_i ∈ [−1, 1]; the last agent evades:
+ *        H = Σ_i a_i (p_xi cos θ_i + p_yi sin θ_i) + |p_θ,A−1| − Σ_{i<A−1} |p_θi|
  *
  *  HJMC_TGT_QUAD_BOWL     any n    params {α0} = {0.25}:   g = |y|²/2 − α0        (config 1)
  *        Dg = x
@@ -79,6 +86,8 @@
  *        Dg = (Δx, Δz, 0, −Δx, −Δz, 0)/ρ;  e1 at ρ = 0
  *  HJMC_TGT_PAIR_UNION    n = 3K   params {r} = {1}:       g = sqrt(min_q (y_{3q}² + y_{3q+1}²)) − r  (R16)
  *        Dg = unit vector of the first minimising pair's position;  e1 at ρ = 0
+ *  HJMC_TGT_PURSUIT_MIN   n = 3A   params {r} = {1.5}:  g = min_{i<A−1} ‖pos_i − pos_{A−1}‖ − r
+ *        Dg = ±unit vector of the first minimising pursuer–evader pair;  e1 at ρ = 0
  *  HJMC_TGT_LINEAR        any n    params {a_0..a_{n−1}, b}: g = a·y + b,  Dg = a     (test target)
  *  HJMC_TGT_CONST         any n    params {k}:             g = k,  Dg = 0              (test target)
  *
@@ -145,6 +154,9 @@ extern "C" {
 #define HJMC_SYS_DUBINS_REL 1
 #define HJMC_SYS_ROCKET6 2
 #define HJMC_SYS_DUBINS_PAIRS 3
+#define HJMC_SYS_ROCKET3 4
+#define HJMC_SYS_DOUBLE_INTEGRATOR 5
+#define HJMC_SYS_MULTIAGENT 6
 
 /* Targets (terminal costs g). */
 #define HJMC_TGT_QUAD_BOWL 0
@@ -153,6 +165,11 @@ extern "C" {
 #define HJMC_TGT_PAIR_UNION 3
 #define HJMC_TGT_LINEAR 4
 #define HJMC_TGT_CONST 5
+#define HJMC_TGT_PURSUIT_MIN 6
+
+/* BRAT avoid sets. */
+#define HJMC_AVOID_NONE 0
+#define HJMC_AVOID_DISK 1
 
 #define HJMC_MAX_N 64            /* state dimension limit of this build                    */
 #define HJMC_MAX_PARAMS 72       /* max float parameters of a system or target             */
@@ -208,6 +225,11 @@ HJMC_API int hjmc_set_dynamics(hjmc_handle* h, int32_t system_id, const float* p
 /* Select the terminal cost g (see TARGETS above). HJMC_EUNSUPPORTED if no kernel exists for
  * (target, n); HJMC_EINVAL for a bad id / np / n. */
 HJMC_API int hjmc_set_target(hjmc_handle* h, int32_t target_id, const float* params, int32_t np);
+
+/* Reach–avoid (BRAT, Eq. HJI-RCBRAT-Visc): avoid function ℓ(x) > 0 inside the
+ * obstacle; the tube becomes max(tube, ℓ(x)). HJMC_AVOID_DISK params
+ * {c0, c1, r}: ℓ(x) = r − ‖(x0 − c0, x1 − c1)‖. HJMC_AVOID_NONE (default) restores the BRT. */
+HJMC_API int hjmc_set_avoid(hjmc_handle* h, int32_t avoid_id, const float* params, int32_t np);
 
 /* 1 if a kernel for (target_id, n) is compiled in, else 0. */
 HJMC_API int hjmc_supported(int32_t target_id, int32_t n);

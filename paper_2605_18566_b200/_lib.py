@@ -13,8 +13,11 @@ LIB_PATH = os.path.join(HERE, "libhjmc.so")
 
 HJMC_OK, HJMC_EINVAL, HJMC_ENUMERIC, HJMC_ECUDA, HJMC_EUNSUPPORTED, HJMC_ENOMEM = range(6)
 ERROR_NAMES = {0: "OK", 1: "EINVAL", 2: "ENUMERIC", 3: "ECUDA", 4: "EUNSUPPORTED", 5: "ENOMEM"}
-SYSTEMS = {"quadratic": 0, "dubins_rel": 1, "rocket6": 2, "dubins_pairs": 3}
-TARGETS = {"quad_bowl": 0, "disk": 1, "rel_disk6": 2, "pair_union": 3, "linear": 4, "const": 5}
+SYSTEMS = {"quadratic": 0, "dubins_rel": 1, "rocket6": 2, "dubins_pairs": 3, "rocket3": 4,
+           "double_integrator": 5, "multiagent": 6}
+TARGETS = {"quad_bowl": 0, "disk": 1, "rel_disk6": 2, "pair_union": 3, "linear": 4, "const": 5,
+           "pursuit_min": 6}
+AVOIDS = {"none": 0, "disk": 1}
 VISC = {"paper": 0, "full": 1}
 FLAG_SYNC_CHECK = 1
 FLAG_SKIP_STATIONARY = 2
@@ -24,7 +27,7 @@ EXPORTS = [
     "hjmc_supported", "hjmc_value_grad", "hjmc_solve_slice", "hjmc_solve_slice_host",
     "hjmc_eval_target", "hjmc_eval_hamiltonian", "hjmc_debug_normals", "hjmc_check",
     "hjmc_last_bad_query", "hjmc_last_error", "hjmc_residual_partials", "hjmc_version",
-    "hjmc_pass_count", "hjmc_picard_begin", "hjmc_picard_pass",
+    "hjmc_pass_count", "hjmc_picard_begin", "hjmc_picard_pass", "hjmc_set_avoid",
 ]
 
 
@@ -83,6 +86,7 @@ def load(path: str = LIB_PATH):
     L.hjmc_residual_partials.argtypes = [vp, vp, C.c_int32, C.c_int32, i64, vp]
     L.hjmc_version.argtypes = []
     L.hjmc_pass_count.argtypes = [vp, vp, C.POINTER(C.c_uint64)]
+    L.hjmc_set_avoid.argtypes = [vp, C.c_int32, C.POINTER(C.c_float), C.c_int32]
     L.hjmc_picard_begin.argtypes = [vp, vp, vp, u32, i64, vp, vp]
     L.hjmc_picard_pass.argtypes = [vp, C.c_int32, vp, vp, vp, vp, vp, vp]
     for name in EXPORTS:

@@ -22,6 +22,7 @@ struct hjmc_handle {
   SystemParams sp{};
   TargetParams tp{};
   int tgt_id = -1;
+  AvoidParams avoid{};
   KernelSet ks{};
   int* d_err = nullptr;
   unsigned long long* d_bad = nullptr;
@@ -228,6 +229,18 @@ int hjmc_set_dynamics(hjmc_handle* h, int32_t id, const float* params, int32_t n
       if (n % 3 != 0) return fail(h, HJMC_EINVAL, "DUBINS_PAIRS needs n = 3K");
       want = 3;
       break;
+    case HJMC_SYS_ROCKET3:
+      if (n != 3) return fail(h, HJMC_EINVAL, "ROCKET3 needs n == 3");
+      want = 2;
+      break;
+    case HJMC_SYS_DOUBLE_INTEGRATOR:
+      if (n != 2) return fail(h, HJMC_EINVAL, "DOUBLE_INTEGRATOR needs n == 2");
+      want = 0;
+      break;
+    case HJMC_SYS_MULTIAGENT:
+      if (n % 3 != 0 || n < 6) return fail(h, HJMC_EINVAL, "MULTIAGENT needs n = 3A, A >= 2");
+      want = 2;
+      break;
     default: return fail(h, HJMC_EINVAL, "unknown system id");
   }
   if (np != 0 && np != want) return fail(h, HJMC_EINVAL, "wrong number of system parameters");
@@ -242,6 +255,26 @@ int hjmc_set_dynamics(hjmc_handle* h, int32_t id, const float* params, int32_t n
   }
   h->sp = sp;
   h->sys_set = true;
+  return HJMC_OK;
+}
+
+int hjmc_set_avoid(hjmc_handle* h, int32_t id, const float* params, int32_t np) {
+  if (!h) return HJMC_EINVAL;
+  AvoidParams a{};
+  if (id == HJMC_AVOID_NONE) {
+    if (np != 0) return fail(h, HJMC_EINVAL, "AVOID_NONE takes no parameters");
+  } else if (id == HJMC_AVOID_DISK) {
+    if (np != 3 || !params) return fail(h, HJMC_EINVAL, "AVOID_DISK needs {c0, c1, r}");
+    if (h->cfg.n < 2) return fail(h, HJMC_EINVAL, "AVOID_DISK needs n >= 2");
+    for (int i = 0; i < 3; ++i) {
+      if (!std::isfinite(params[i])) return fail(h, HJMC_EINVAL, "non-finite avoid parameter");
+      a.p[i] = params[i];
+    }
+  } else {
+    return fail(h, HJMC_EINVAL, "unknown avoid id");
+  }
+  a.type = id;
+  h->avoid = a;
   return HJMC_OK;
 }
 
@@ -267,6 +300,9 @@ int hjmc_set_target(hjmc_handle* h, int32_t id, const float* params, int32_t np)
       break;
     case HJMC_TGT_LINEAR:
       want_min = want_max = n + 1;
+      break;
+    case HJMC_TGT_PURSUIT_MIN:
+      if (n % 3 != 0 || n < 6) return fail(h, HJMC_EINVAL, "PURSUIT_MIN needs n = 3A, A >= 2");
       break;
     case HJMC_TGT_CONST: break;
     default: return fail(h, HJMC_EINVAL, "unknown target id");
@@ -368,7 +404,7 @@ int hjmc_solve_slice(hjmc_handle* h, const float* x, const uint32_t* qid, uint32
   cudaError_t e = h->ks.solve(p, units, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "solve launch");
   if (want_tube) {
-    e = launch_tube(g0, vfinal, h->cfg.K, M, out->tube, s);
+    e = launch_tube(g0, vfinal, h->cfg.K, M, out->tube, x, h->cfg.n, h->avoid, s);
     if (e != cudaSuccess) return cuda_fail(h, e, "tube launch");
   }
   return sync_check_if_requested(h, s);

@@ -10,11 +10,16 @@ namespace hjmc {
 namespace {
 
 __global__ void tube_kernel(const float* __restrict__ g0, const float* __restrict__ vfinal, int K,
-                            int64_t M, float* __restrict__ tube) {
+                            int64_t M, float* __restrict__ tube, const float* __restrict__ x,
+                            int n, AvoidParams avoid) {
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
   float t = g0[m];  // running min including g
   for (int j = 0; j < K; ++j) t = fminf(t, vfinal[(size_t)j * (size_t)M + (size_t)m]);
+  if (avoid.type == 1) {  // BRAT clamp: exclude the obstacle
+    const double dx = (double)x[m * n] - avoid.p[0], dy = (double)x[m * n + 1] - avoid.p[1];
+    t = fmaxf(t, (float)((double)avoid.p[2] - sqrt(dx * dx + dy * dy)));
+  }
   tube[m] = t;
 }
 
@@ -100,9 +105,9 @@ cudaError_t launch_picard_residual(const float* v, float* v_prev, int64_t M, con
 }
 
 cudaError_t launch_tube(const float* g0, const float* vfinal, int K, int64_t M, float* tube,
-                        cudaStream_t s) {
+                        const float* x, int n, AvoidParams avoid, cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
-  tube_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(g0, vfinal, K, M, tube);
+  tube_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(g0, vfinal, K, M, tube, x, n, avoid);
   return cudaGetLastError();
 }
 

@@ -88,8 +88,15 @@ struct KernelSet {
 // (target id, n) → compiled kernels; false if not instantiated.
 bool lookup_kernels(int target, int n, KernelSet* out);
 
+// BRAT avoid set: type 0 none, 1 disk {c0, c1, r}: ℓ(x) = r − ‖(x0 − c0, x1 − c1)‖.
+struct AvoidParams {
+  int type;
+  float p[3];
+};
+
+// tube[m] = max(min(g0[m], min_j vfinal[j][m]), ℓ(x_m))  (running-min BRT; BRAT clamp)
 cudaError_t launch_tube(const float* g0, const float* vfinal, int K, int64_t M, float* tube,
-                        cudaStream_t s);
+                        const float* x, int n, AvoidParams avoid, cudaStream_t s);
 cudaError_t launch_hamiltonian(const EvalParams& p, cudaStream_t s);
 // Per active horizon a (grid y) and block b (grid x): partial[a][b] = (Σ (v−v_prev)², Σ v_prev²,
 // max |v−v_prev|) over that block's queries; then v_prev ← v. Deterministic (fixed order).

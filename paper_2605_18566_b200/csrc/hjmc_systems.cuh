@@ -9,7 +9,10 @@
 
 namespace hjmc {
 
-enum : int { kSysQuadratic = 0, kSysDubinsRel = 1, kSysRocket6 = 2, kSysDubinsPairs = 3 };
+enum : int {
+  kSysQuadratic = 0, kSysDubinsRel = 1, kSysRocket6 = 2, kSysDubinsPairs = 3, kSysRocket3 = 4,
+  kSysDoubleIntegrator = 5, kSysMultiAgent = 6
+};
 
 struct SystemParams {
   int id;
@@ -51,6 +54,28 @@ __device__ inline double hamiltonian(const SystemParams& s, const double* x, con
         h += a * (p[3 * v] * cs + p[3 * v + 1] * sn) - grav * p[3 * v + 1];
       }
       return h - fabs(p[2]) + fabs(p[5]) + dmax * sqrt(p[3] * p[3] + p[4] * p[4]);
+    }
+    case kSysRocket3: {  // Eq. rocket_ham_simplified verbatim (R14)
+      const double a = sys_param(s, 0, 64.0), grav = sys_param(s, 1, 32.0);
+      double sn, cs;
+      sincos(x[2], &sn, &cs);
+      return -(a * p[0] * cs + p[1] * (a + a * sn - grav) - fabs(p[0] * x[0] + p[2]) -
+               fabs(p[1] * x[0] - p[2]));
+    }
+    case kSysDoubleIntegrator:  // Eq. dint_ham, u = −sign(p2)
+      return p[0] * x[1] - fabs(p[1]);
+    case kSysMultiAgent: {  // last agent evades (+|p_θ|), the others pursue (−|p_θ|)
+      const int A = n / 3;
+      const double ap = sys_param(s, 0, 1.0), ae = sys_param(s, 1, 1.0);
+      double h = 0.0;
+      for (int i = 0; i < A; ++i) {
+        double sn, cs;
+        sincos(x[3 * i + 2], &sn, &cs);
+        const double a = (i == A - 1) ? ae : ap;
+        h += a * (p[3 * i] * cs + p[3 * i + 1] * sn);
+        h += (i == A - 1) ? fabs(p[3 * i + 2]) : -fabs(p[3 * i + 2]);
+      }
+      return h;
     }
     case kSysDubinsPairs: {  // R16: decoupled relative Dubins pairs
       const double vp = sys_param(s, 0, 5.0), ve = sys_param(s, 1, 5.0), w = sys_param(s, 2, 1.0);

@@ -173,6 +173,68 @@ struct PairUnion {  // g = sqrt(min_q (y_{3q}² + y_{3q+1}²)) − r  (n = 3K)
 
 // ---------------------------------------------------------------------------------------------
 template <int NDIM>
+struct PursuitMin {  // g = min_{i < A−1} ‖pos_i − pos_{A−1}‖ − r  (n = 3A)
+  static_assert(NDIM % 3 == 0 && NDIM >= 6, "PURSUIT_MIN needs n = 3A, A >= 2");
+  static constexpr int kAgents = NDIM / 3;
+  static constexpr int kE = 3 * (kAgents - 1);  // evader's first coordinate
+  float off;
+  __device__ explicit PursuitMin(const TargetParams& t) : off(-(t.np > 0 ? t.p[0] : 1.5f)) {}
+  __device__ __forceinline__ float core(const float (&xs)[NDIM], float sigma,
+                                        const float (&z)[NDIM]) const {
+    const float ex = fmaf(sigma, z[kE], xs[kE]);
+    const float ey = fmaf(sigma, z[kE + 1], xs[kE + 1]);
+    float best = 3.0e38f;
+#pragma unroll
+    for (int i = 0; i < kAgents - 1; ++i) {
+      const float dx = fmaf(sigma, z[3 * i], xs[3 * i]) - ex;
+      const float dy = fmaf(sigma, z[3 * i + 1], xs[3 * i + 1]) - ey;
+      best = fminf(best, fmaf(dx, dx, dy * dy));
+    }
+    return sqrt_approx(best);
+  }
+  __device__ float core_lower(const float (&xs)[NDIM], float sigma) const {
+    float best = 3.0e38f;
+    for (int i = 0; i < kAgents - 1; ++i) {
+      const float dx = xs[3 * i] - xs[kE], dy = xs[3 * i + 1] - xs[kE + 1];
+      best = fminf(best, dx * dx + dy * dy);
+    }
+    return fmaxf(0.f, sqrtf(best) - 2.f * sigma * kZmax2) * 0.9999f;
+  }
+  __device__ double g_host(const double* x) const {
+    double best = 1e300;
+    for (int i = 0; i < kAgents - 1; ++i) {
+      const double dx = x[3 * i] - x[kE], dy = x[3 * i + 1] - x[kE + 1];
+      const double d = sqrt(dx * dx + dy * dy);
+      best = d < best ? d : best;
+    }
+    return best + (double)off;
+  }
+  __device__ void dg(const double* x, double* g) const {
+    for (int d = 0; d < NDIM; ++d) g[d] = 0.0;
+    double best = 1e300;
+    int arg = 0;
+    for (int i = 0; i < kAgents - 1; ++i) {
+      const double dx = x[3 * i] - x[kE], dy = x[3 * i + 1] - x[kE + 1];
+      const double d = sqrt(dx * dx + dy * dy);
+      if (d < best) {  // first minimiser on ties
+        best = d;
+        arg = i;
+      }
+    }
+    if (best > 0.0) {
+      const double ux = (x[3 * arg] - x[kE]) / best, uy = (x[3 * arg + 1] - x[kE + 1]) / best;
+      g[3 * arg] = ux;
+      g[3 * arg + 1] = uy;
+      g[kE] = -ux;
+      g[kE + 1] = -uy;
+    } else {
+      g[0] = 1.0;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------------------------
+template <int NDIM>
 struct Linear {  // g = a·y + b (test target; Gaussian-tilt identities)
   float a[NDIM];
   float off;

@@ -37,13 +37,15 @@ class SolverConfig:
     sys_params: tuple = ()
     target: str = "quad_bowl"
     tgt_params: tuple = ()
+    avoid: str = "none"
+    avoid_params: tuple = ()
 
     @classmethod
     def from_preset(cls, p: Preset, **kw) -> "SolverConfig":
         d = dict(n=p.n, delta=p.delta, T=p.T, K=p.K, Kp=p.Kp, N=p.N, seed=p.seed, visc=p.visc,
                  crn=p.crn, antithetic=p.antithetic, m0=p.m0, c_min=p.c_min, c_max=p.c_max,
                  tag=p.tag, system=p.system, sys_params=tuple(p.sys_params), target=p.target,
-                 tgt_params=tuple(p.tgt_params))
+                 tgt_params=tuple(p.tgt_params), avoid=p.avoid, avoid_params=tuple(p.avoid_params))
         d.update(kw)
         return cls(**d)
 
@@ -86,6 +88,9 @@ class Solver:
         self._check(self.L.hjmc_set_dynamics(self.h, _lib.SYSTEMS[cfg.system], arr, np_))
         arr, np_ = _floats(cfg.tgt_params)
         self._check(self.L.hjmc_set_target(self.h, _lib.TARGETS[cfg.target], arr, np_))
+        if cfg.avoid != "none":
+            arr, np_ = _floats(cfg.avoid_params)
+            self._check(self.L.hjmc_set_avoid(self.h, _lib.AVOIDS[cfg.avoid], arr, np_))
 
     # -- plumbing --------------------------------------------------------------------------
     def _check(self, rc, h="self"):

@@ -351,3 +351,46 @@ def test_full_size_configs_golden(O, idx):
     assert_dv(out["dv"], ref["dv"])
     assert_v(out["tube"], ref["tube"], "tube")
     np.testing.assert_allclose(out["g0"], ref["g0"], rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("preset,n_q,kw", [
+    ("paper_rockets3_40x40", 49, dict(N=3000, K=2, Kp=4)),
+    ("paper_double_integrator", 49, dict(N=3000, K=2, Kp=4)),
+    ("paper_multiagent45", 16, dict(N=800, K=2, Kp=3)),
+])
+def test_solve_slice_paper_systems(O, preset, n_q, kw):
+    """The paper's own systems through the fused kernel vs oracle."""
+    p = I.PRESETS[preset].with_(**kw)
+    s = Solver(SolverConfig.from_preset(p))
+    x = I.queries(p)
+    x = x[np.linspace(0, x.shape[0] - 1, n_q).round().astype(int)]
+    _compare_solve(O, s, O.Problem.from_preset(p), x)
+
+
+def test_multiagent_small_and_hamiltonian(O):
+    s, P = pair(O, n=9, delta=0.02, T=1.0, K=2, Kp=3, N=2000, system="multiagent",
+                sys_params=(1.0, 2.0), target="pursuit_min", tgt_params=(1.5,))
+    x = I.random_queries(9, 25, -4, 4, seed=3)
+    _compare_solve(O, s, P, x)
+    rng = np.random.default_rng(1)
+    xx = rng.uniform(-3, 3, (30, 9)).astype(np.float32)
+    pp = rng.normal(size=(30, 9)).astype(np.float32)
+    H, _ = s.eval_hamiltonian(xx, pp)
+    Ho = [O.hamiltonian(P, xx[m].astype(float), pp[m].astype(float)) for m in range(30)]
+    np.testing.assert_allclose(H.cpu().numpy(), Ho, rtol=1e-6, atol=1e-5)
+
+
+def test_brat_clamp_gpu(O):
+    """HJI-RCBRAT-Visc: tube = max(BRT tube, ℓ(x)) with a disk obstacle."""
+    p = I.PAPER_DOUBLE_INTEGRATOR.with_(N=2000, K=2, Kp=3)
+    x = I.queries(p)[::7]
+    brt = Solver(SolverConfig.from_preset(p)).solve_slice(x)
+    pa = p.with_(avoid="disk", avoid_params=(0.3, -0.2, 0.4))
+    s = Solver(SolverConfig.from_preset(pa))
+    brat = s.solve_slice(x)
+    P = O.Problem.from_preset(pa)
+    ell = np.array([O.avoid_l(P, xm.astype(np.float64)) for xm in x])
+    np.testing.assert_allclose(brat["tube"].cpu().numpy(),
+                               np.maximum(brt["tube"].cpu().numpy(), ell), rtol=0, atol=1e-6)
+    assert torch.equal(brat["v"], brt["v"])
+    _compare_solve(O, s, P, x, hist_check=False)
