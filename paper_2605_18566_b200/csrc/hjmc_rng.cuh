@@ -73,30 +73,30 @@ __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
   return make_uint4(c0, c1, c2, c3);
 }
 
-// m = w >> 9 (high 23 bits). 0x3F800000 + m is the float 1 + m·2^-23 (one LEA.HI / IADD):
+// m = w >> 9 (high 23 bits). 0x3F800000 + m is the float 1 + m·2^-23 = 1 + a(w) (one LEA.HI):
 //   u(w) = (2m+1)·2^-24 = (1 + m·2^-23) − (1 − 2^-24)   exact (both operands in [0.5, 2))
-//   a(w) − ½ = (1 + m·2^-23) − 1.5                      exact
 __device__ __forceinline__ float mantissa_float(uint32_t w) {
   return __uint_as_float((w >> 9) + 0x3F800000u);
 }
 __device__ __forceinline__ float unif_open(uint32_t w) {
   return mantissa_float(w) - 0.99999994039535522f;  // 1 − 2^-24
 }
-__device__ __forceinline__ float unif_angle_centered(uint32_t w) { return mantissa_float(w) - 1.5f; }
 
-// Box–Muller scaled by 1/C, C = −sqrt(2 ln 2): returns ẑ with z = C·ẑ, i.e.
-//   ẑ_cos = sqrt(−log2 u)·cos(2π(a − ½)),  ẑ_sin = sqrt(−log2 u)·sin(2π(a − ½)),
-// since r cos(2πa) = sqrt(−2 ln2 · log2 u)·(−cos(2π(a − ½))) = C·ẑ_cos (same for sin).
+// Box–Muller scaled by 1/C, C = sqrt(2 ln 2): returns ẑ with z = C·ẑ, i.e.
+//   ẑ_cos = sqrt(−log2 u)·cos(2π(1 + a)),  ẑ_sin = sqrt(−log2 u)·sin(2π(1 + a)),
+// since r = sqrt(−2 ln u) = C·sqrt(−log2 u) and sin/cos are 2π-periodic, so the angle is
+// formed straight from the mantissa float 1 + a (no centring add); MUFU.SIN/COS take their
+// argument in revolutions, so 2π(1+a)·(1/2π) ∈ [1, 2) keeps the full 2^-23 angle resolution.
 // The caller folds C into σ (y = x + (σC)·ẑ) and into the moment epilogue, which saves one
 // multiply per pair. kNeedSin = false skips the sin (odd n: last normal of the quad unused).
-constexpr float kBMScale = -1.1774100225154747f;  // −sqrt(2 ln 2)
+constexpr float kBMScale = 1.1774100225154747f;  // sqrt(2 ln 2)
 
 template <bool kNeedSin = true>
 __device__ __forceinline__ void box_muller_hat(uint32_t w_r, uint32_t w_a, float& zc, float& zs) {
   constexpr float kTwoPi = 6.2831853071795865f;
   // log2 u < 0 for every u < 1; |·| guards the MUFU rounding sign near u = 1 (free modifier)
   const float rh = sqrt_approx(fabsf(lg2_approx(unif_open(w_r))));
-  const float th = kTwoPi * unif_angle_centered(w_a);
+  const float th = kTwoPi * mantissa_float(w_a);
   zc = rh * cos_approx(th);
   if (kNeedSin) zs = rh * sin_approx(th);
 }
