@@ -106,6 +106,23 @@ __device__ __forceinline__ uint32_t ctr_word1(uint32_t b, uint32_t kw, uint32_t 
   return b | (kw << 8) | (jw << 16);
 }
 
+// ẑ of quads B.. of a sample from their Philox words (compile-time recursion over quads).
+template <int NDIM, int B = 0>
+__device__ __forceinline__ void normals_from_words(float (&z)[NDIM],
+                                                   const uint4 (&w)[(NDIM + 3) / 4]) {
+  constexpr int d = 4 * B;
+  float t0, t1, t2, t3;
+  box_muller_hat<(d + 1 < NDIM)>(w[B].x, w[B].y, t0, t1);
+  z[d] = t0;
+  if constexpr (d + 1 < NDIM) z[d + 1] = t1;
+  if constexpr (d + 2 < NDIM) {
+    box_muller_hat<(d + 3 < NDIM)>(w[B].z, w[B].w, t2, t3);
+    z[d + 2] = t2;
+    if constexpr (d + 3 < NDIM) z[d + 3] = t3;
+  }
+  if constexpr (B + 1 < (NDIM + 3) / 4) normals_from_words<NDIM, B + 1>(z, w);
+}
+
 // ẑ of one quad from its Philox words (the first min(NDIM, 4) coordinates).
 template <int NDIM>
 __device__ __forceinline__ void quad_normals_hat(float (&z)[NDIM], uint4 w) {

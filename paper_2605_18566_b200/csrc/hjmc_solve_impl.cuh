@@ -96,6 +96,94 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
   }
 }
 
+#ifndef HJMC_WS
+#define HJMC_WS 0
+#endif
+#ifndef HJMC_WS_STAGES
+#define HJMC_WS_STAGES 4
+#endif
+#ifndef HJMC_WS_SPT
+#define HJMC_WS_SPT 2
+#endif
+constexpr int kWsStages = HJMC_WS_STAGES;   // ring depth
+constexpr int kWsSpt = HJMC_WS_SPT;         // samples per thread per stage
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Warp-specialised Φ pass (non-antithetic): warps 0..NT/64−1 produce the Philox words of each
+// stage's samples into a shared-memory ring (integer-multiply + logic pipes); the other half
+// consume them (Box–Muller on MUFU + FP32, target, weight, moments). Each SMSP hosts one
+// producer and one consumer warp per CTA, so both pipe groups stay busy whatever phase the
+// warps are in. Stage t ↔ samples t·B .. t·B + B − 1 (B = kWsSpt·NT/2); FULL(s)/EMPTY(s) are
+// named barriers 1..2·kWsStages over all NT threads (producers arrive/sync, consumers sync/
+// arrive). Consumers skip EMPTY for the last kWsStages stages, which no producer waits for,
+// so every barrier instance is balanced at the end of the pass.
+template <int NDIM>
+struct WsRing {
+  static constexpr int kQuads = (NDIM + 3) / 4;
+  uint4 w[kWsStages][kWsSpt][128][kQuads];
+};
+
+template <class Tgt, int NDIM, int NT>
+__device__ __forceinline__ void mc_accumulate_ws(WsRing<NDIM>& ring, const Tgt& tgt,
+                                                 const float (&xs)[NDIM], float sigma, float A,
+                                                 float B, uint32_t N, uint32_t w1base,
+                                                 uint32_t qid, uint32_t tag, const RoundKeys& rk,
+                                                 float& S, float (&Mz)[NDIM]) {
+  static_assert(NT == 256, "ring layout assumes 128 producers + 128 consumers");
+  constexpr int kHalf = NT / 2;
+  constexpr int kStage = kWsSpt * kHalf;
+  constexpr int kQuads = WsRing<NDIM>::kQuads;
+  S = 0.f;
+#pragma unroll
+  for (int d = 0; d < NDIM; ++d) Mz[d] = 0.f;
+  const uint32_t stages = (N + kStage - 1) / kStage;
+  const bool producer = threadIdx.x < kHalf;
+  const int t0 = producer ? threadIdx.x : threadIdx.x - kHalf;
+  if (producer) {
+    for (uint32_t t = 0; t < stages; ++t) {
+      const int st = (int)(t % kWsStages);
+      if (t >= kWsStages) named_bar_sync(1 + kWsStages + st, NT);  // EMPTY(st)
+#pragma unroll
+      for (int e = 0; e < kWsSpt; ++e) {
+        const uint32_t i = t * kStage + e * kHalf + t0;
+        if (i < N) {
+#pragma unroll
+          for (int b = 0; b < kQuads; ++b)
+            ring.w[st][e][t0][b] = philox4x32_10(i, w1base | (uint32_t)b, qid, tag, rk);
+        }
+      }
+      named_bar_arrive(1 + st, NT);                                   // FULL(st)
+    }
+  } else {
+    for (uint32_t t = 0; t < stages; ++t) {
+      const int st = (int)(t % kWsStages);
+      named_bar_sync(1 + st, NT);                                     // FULL(st)
+#pragma unroll
+      for (int e = 0; e < kWsSpt; ++e) {
+        const uint32_t i = t * kStage + e * kHalf + t0;
+        if (i < N) {
+          uint4 wq[kQuads];
+#pragma unroll
+          for (int b = 0; b < kQuads; ++b) wq[b] = ring.w[st][e][t0][b];
+          float z[NDIM];
+          normals_from_words<NDIM>(z, wq);
+          const float wt = ex2_approx(fmaf(A, tgt.core(xs, sigma, z), B));
+          S += wt;
+#pragma unroll
+          for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(wt, z[d], Mz[d]);
+        }
+      }
+      if (t + kWsStages < stages) named_bar_arrive(1 + kWsStages + st, NT);  // EMPTY(st)
+    }
+  }
+}
+
 // Largest exponent A·core(y_i) over this thread's samples (fallback shift; rarely used).
 template <class Tgt, int NDIM, int NT>
 __device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float sigma, float A,
@@ -266,6 +354,7 @@ constexpr int min_blocks() {
 template <class Tgt, int NDIM, int NT>
 __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __grid_constant__ SolveParams P) {
   __shared__ SolveSmem<NDIM, NT> sm;
+  __shared__ WsRing<(HJMC_WS && NDIM <= 8) ? NDIM : 1> ring;
   const int64_t unit = blockIdx.x;
   int64_t m;
   int j;
@@ -323,8 +412,17 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __g
     float B = -A * lowc;  // every a_i = A core_i + B ≤ 0: no weight can overflow
 
     float S, Mz[NDIM];
-    mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id, P.tag,
-                                 P.rk, S, Mz);
+    if constexpr (HJMC_WS && NT == 256 && NDIM <= 8) {
+      if (!P.antithetic)
+        mc_accumulate_ws<Tgt, NDIM, NT>(ring, tgt, xs, sigma_s, A, B, P.N, w1base, id, P.tag,
+                                        P.rk, S, Mz);
+      else
+        mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id,
+                                     P.tag, P.rk, S, Mz);
+    } else {
+      mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id, P.tag,
+                                   P.rk, S, Mz);
+    }
     cta_reduce<NDIM, NT>(sm, S, Mz);
     if (!(sm.sum[0] >= (double)kUnderflowS)) {
       // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with

@@ -8,13 +8,11 @@ sys.path.insert(0, ROOT)
 from paper_2605_18566_b200 import build as B  # noqa: E402
 
 VARIANTS = {
-    "a_base": [],
-    "b_swp": ["-DHJMC_SWP=1"],
-    "c_unroll1": ["-DHJMC_UNROLL=1"],
-    "d_unroll4": ["-DHJMC_UNROLL=4"],
-    "e_mb5": ["-DHJMC_MINB=5"],
-    "f_swp_mb5": ["-DHJMC_SWP=1", "-DHJMC_MINB=5"],
-    "g_nt128": ["-DHJMC_NT=128", "-DHJMC_MINB=8"],
+    "a_ws0": ["-DHJMC_WS=0"],
+    "b_ws_s4_p1": ["-DHJMC_WS=1", "-DHJMC_WS_STAGES=4", "-DHJMC_WS_SPT=1"],
+    "c_ws_s8_p1": ["-DHJMC_WS=1", "-DHJMC_WS_STAGES=8", "-DHJMC_WS_SPT=1"],
+    "d_ws_s2_p4": ["-DHJMC_WS=1", "-DHJMC_WS_STAGES=2", "-DHJMC_WS_SPT=4"],
+    "e_ws_s6_p2": ["-DHJMC_WS=1", "-DHJMC_WS_STAGES=6", "-DHJMC_WS_SPT=2"],
 }
 
 if __name__ == "__main__":
