@@ -45,17 +45,21 @@
  *    round (c0,c1,c2,c3) → ( hi(M1·c2) ^ c1 ^ k0,  lo(M1·c2),  hi(M0·c0) ^ c3 ^ k1,  lo(M0·c0) )
  *          M0 = 0xD2511F53, M1 = 0xCD9E8D57; after each of the first 9 rounds
  *          k0 += 0x9E3779B9, k1 += 0xBB67AE85; the output (x0,x1,x2,x3) is the 10th round's.
- *  Counter of sample i, coordinate quad b = d/4 (d = 0..n−1):
- *    c0 = i            (antithetic: c0 = i >> 1, and odd i use −z)
- *    c1 = b | (kw << 8) | (jw << 16)
+ *  Draw layout (which Philox block feeds which normal): draw q = i (antithetic: q = i >> 1,
+ *  odd i use −z). Let G = 4/gcd(n, 4) if G·n ≤ 16, else G = 1; Q = G·n/4 (G > 1) or ceil(n/4)
+ *  (G = 1). Draw group γ = q / G has blocks b = 0..Q−1 whose Box–Muller outputs form one flat
+ *  stream; draw q's normal d is stream element (q mod G)·n + d (G = 1: element d). Block b of
+ *  group γ is Philox with counter
+ *    c0 = γ,   c1 = b | (kw << 8) | (jw << 16),   c2 = global query id,   c3 = tag
  *         solve_slice: jw = j (1..K), kw = crn ? 0 : k (0..Kp−1);  value_grad: caller's tags
- *    c2 = global query id;   c3 = config tag
+ *  (n = 2, 3, 6 thus use every normal a Philox call makes; the Q blocks of a group share the
+ *  first Philox rounds, which depend on c0 but not on b.)
  *  Uniforms from a 32-bit word w:  m = w >> 9 (its high 23 bits);
  *    u(w) = (2m + 1) · 2^−24  ∈ (0, 1)       (radius argument, never 0 or 1)
  *    a(w) = m · 2^−23          ∈ [0, 1)       (angle fraction)
- *  Box–Muller, per Philox output (x0, x1, x2, x3) of quad b:
- *    r = sqrt(−2 ln u(x0)):  z_{4b}   = r cos(2π a(x1)),  z_{4b+1} = r sin(2π a(x1))
- *    r'= sqrt(−2 ln u(x2)):  z_{4b+2} = r'cos(2π a(x3)),  z_{4b+3} = r'sin(2π a(x3))
+ *  Box–Muller, per block output (x0, x1, x2, x3) → stream elements 4t .. 4t+3 of the block's slot t:
+ *    r = sqrt(−2 ln u(x0)):  ζ_{4t}   = r cos(2π a(x1)),  ζ_{4t+1} = r sin(2π a(x1))
+ *    r'= sqrt(−2 ln u(x2)):  ζ_{4t+2} = r'cos(2π a(x3)),  ζ_{4t+3} = r'sin(2π a(x3))
  *  Hence |z_d| ≤ sqrt(48 ln 2) = 5.7683 for every coordinate.
  *
  * ----------------------------------------------------------------------------------------
@@ -291,7 +295,8 @@ HJMC_API int hjmc_eval_hamiltonian(hjmc_handle* h, const float* x, const float* 
 
 /* The sampled normals exactly as the kernels generate them, for RNG parity tests:
  * z[s][n] (dev) for samples i = i0 .. i0+count−1 of query qid with counter tags (jw, kw);
- * raw[s][4·ceil(n/4)] (dev, may be NULL) receives the Philox words. Antithetic sign applies. */
+ * raw[s][4·(ceil(n/4)+1)] (dev, may be NULL) receives the words of every Philox block the
+ * sample touches, in order (unused tail entries untouched). Antithetic sign applies. */
 HJMC_API int hjmc_debug_normals(hjmc_handle* h, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
                        uint32_t count, float* z, uint32_t* raw, void* stream);
 

@@ -154,7 +154,7 @@ def philox(ctr, key):
 
 def normals(P: Problem, qid: int, jw: int, kw: int, i0: int, count: int, raw: bool = False):
     s = P.struct()
-    nq = (P.n + 3) // 4
+    nq = (P.n + 3) // 4 + 1                      # blocks a sample can touch (R19 grouping)
     z = np.zeros((count, P.n))
     r = np.zeros((count, 4 * nq), dtype=np.uint32)
     for t in range(count):

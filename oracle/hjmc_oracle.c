@@ -47,31 +47,58 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
 static double unif_open(uint32_t w) { return (2.0 * (double)(w >> 9) + 1.0) / 16777216.0; }
 static double unif_angle(uint32_t w) { return (double)(w >> 9) / 8388608.0; }
 
-/* The n standard normals z_{i,0..n-1} of sample i ("y_i ~ N(0, I_n)"), Box–Muller on
- * Philox words with counter (i, b | kw<<8 | jw<<16, qid, tag), b = quad index (R19). */
-void orc_sample_normals(const orc_problem* P, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i,
-                        double* z, uint32_t* raw) {
+/* Grouping of draws (R19): G = 4/gcd(n,4) consecutive draws share one flat stream of
+ * G*n normals (G*n/4 Philox blocks) when G*n <= 16, else G = 1 and each draw takes
+ * ceil(n/4) blocks of its own. */
+static int draw_group(int n) {
+  int g = (n % 4 == 0) ? 1 : ((n % 2 == 0) ? 2 : 4);
+  return (g * n <= 16) ? g : 1;
+}
+
+/* One Philox block -> its four normals: Box-Muller on word pairs (0,1) and (2,3). */
+static void block_normals(const orc_problem* P, uint32_t group, uint32_t b, uint32_t qid,
+                          uint32_t jw, uint32_t kw, double zz[4], uint32_t w[4]) {
   const double two_pi = 6.283185307179586476925286766559;
   uint32_t key[2] = {(uint32_t)(P->seed & 0xFFFFFFFFu), (uint32_t)(P->seed >> 32)};
+  uint32_t ctr[4] = {group, b | (kw << 8) | (jw << 16), qid, P->tag};
+  orc_philox4x32_10(ctr, key, w);
+  double r01 = sqrt(-2.0 * log(unif_open(w[0])));
+  double r23 = sqrt(-2.0 * log(unif_open(w[2])));
+  zz[0] = r01 * cos(two_pi * unif_angle(w[1]));
+  zz[1] = r01 * sin(two_pi * unif_angle(w[1]));
+  zz[2] = r23 * cos(two_pi * unif_angle(w[3]));
+  zz[3] = r23 * sin(two_pi * unif_angle(w[3]));
+}
+
+/* The n standard normals z_{i,0..n-1} of sample i ("y_i ~ N(0, I_n)"): draw
+ * q = i (antithetic: i >> 1, odd i negated), group g = q / G, r = q mod G; the group's Q
+ * blocks (Q = ceil(n/4) for G = 1, G*n/4 otherwise) b = 0..Q-1 have counter
+ * (g, b | kw << 8 | jw << 16, qid, tag) and their Box-Muller outputs form one stream; normal
+ * d is element l = r*n + d (G = 1: l = d), i.e. word l % 4 of block l / 4 (R19). raw (may be
+ * NULL) receives the 4 words of every block the sample touches, in order. */
+void orc_sample_normals(const orc_problem* P, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i,
+                        double* z, uint32_t* raw) {
+  int n = P->n;
   uint32_t draw = P->antithetic ? (i >> 1) : i;
   double sign = (P->antithetic && (i & 1u)) ? -1.0 : 1.0;
-  int nquads = (P->n + 3) / 4;
-  for (int b = 0; b < nquads; ++b) {
-    uint32_t ctr[4] = {draw, (uint32_t)b | (kw << 8) | (jw << 16), qid, P->tag};
-    uint32_t w[4];
-    orc_philox4x32_10(ctr, key, w);
-    if (raw) for (int t = 0; t < 4; ++t) raw[4 * b + t] = w[t];
-    double r01 = sqrt(-2.0 * log(unif_open(w[0])));
-    double r23 = sqrt(-2.0 * log(unif_open(w[2])));
-    double zz[4];
-    zz[0] = r01 * cos(two_pi * unif_angle(w[1]));
-    zz[1] = r01 * sin(two_pi * unif_angle(w[1]));
-    zz[2] = r23 * cos(two_pi * unif_angle(w[3]));
-    zz[3] = r23 * sin(two_pi * unif_angle(w[3]));
-    for (int t = 0; t < 4; ++t) {
-      int d = 4 * b + t;
-      if (d < P->n) z[d] = sign * zz[t];
+  int G = draw_group(n);
+  uint32_t g = draw / (uint32_t)G;
+  int r = (int)(draw % (uint32_t)G);
+  int first = (G == 1) ? 0 : r * n;                 /* position of normal 0 in the stream */
+  int64_t cur = -1;
+  double zz[4];
+  uint32_t w[4];
+  int nraw = 0;
+  for (int d = 0; d < n; ++d) {
+    int l = first + d;
+    int64_t blk = l / 4;
+    if (blk != cur) {
+      block_normals(P, g, (uint32_t)blk, qid, jw, kw, zz, w);
+      if (raw) { for (int t = 0; t < 4; ++t) raw[4 * nraw + t] = w[t]; }
+      ++nraw;
+      cur = blk;
     }
+    z[d] = sign * zz[l % 4];
   }
 }
 

@@ -36,6 +36,9 @@ __global__ void hamiltonian_kernel(const EvalParams P) {
   if (P.c) P.c[m] = (float)gamma_update(P.sp, P.gp, x, p);
 }
 
+// The sampler's normals exactly as the solve kernels draw them (R19 layout, runtime n): for
+// sample i its draw's group g, position r in the group, and the Philox blocks its n normals
+// come from; raw receives the words of every block the sample touches, in order.
 __global__ void debug_normals_kernel(int n, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
                                      uint32_t count, const __grid_constant__ RoundKeys rk,
                                      uint32_t tag, int antithetic, float* z, uint32_t* raw) {
@@ -44,18 +47,27 @@ __global__ void debug_normals_kernel(int n, uint32_t qid, uint32_t jw, uint32_t 
   const uint32_t i = i0 + s;
   const uint32_t draw = antithetic ? (i >> 1) : i;
   const float sign = (antithetic && (i & 1u)) ? -1.f : 1.f;
-  const int quads = (n + 3) / 4;
-  for (int b = 0; b < quads; ++b) {
-    const uint4 w = philox4x32_10(draw, ctr_word1((uint32_t)b, kw, jw), qid, tag, rk);
-    if (raw) {
-      uint32_t* r = raw + (size_t)s * 4 * quads + 4 * b;
-      r[0] = w.x; r[1] = w.y; r[2] = w.z; r[3] = w.w;
+  const int g0 = (n % 4 == 0) ? 1 : ((n % 2 == 0) ? 2 : 4);
+  const int G = (g0 * n <= 16) ? g0 : 1;
+  const uint32_t grp = draw / (uint32_t)G;
+  const int first = (G == 1) ? 0 : (int)(draw % (uint32_t)G) * n;
+  const int rawmax = 4 * ((n + 3) / 4 + 1);
+  int cur = -1, nraw = 0;
+  float t[4];
+  for (int d = 0; d < n; ++d) {
+    const int l = first + d;
+    if (l / 4 != cur) {
+      cur = l / 4;
+      const uint4 w = philox4x32_10(grp, ctr_word1((uint32_t)cur, kw, jw), qid, tag, rk);
+      if (raw) {
+        uint32_t* r = raw + (size_t)s * rawmax + 4 * nraw;
+        r[0] = w.x; r[1] = w.y; r[2] = w.z; r[3] = w.w;
+      }
+      ++nraw;
+      box_muller_hat<true>(w.x, w.y, t[0], t[1]);
+      box_muller_hat<true>(w.z, w.w, t[2], t[3]);
     }
-    float t[4];
-    box_muller_hat<true>(w.x, w.y, t[0], t[1]);
-    box_muller_hat<true>(w.z, w.w, t[2], t[3]);
-    for (int e = 0; e < 4; ++e)
-      if (4 * b + e < n) z[(size_t)s * n + 4 * b + e] = sign * kBMScale * t[e];
+    z[(size_t)s * n + d] = sign * kBMScale * t[l % 4];
   }
 }
 

@@ -38,6 +38,14 @@ __device__ __forceinline__ float cos_approx(float x) {
   return y;
 }
 
+// Hide a value's provenance from the optimiser so a loop-invariant stays in a register instead of
+// being re-derived inside the sample loop (e.g. a double→float conversion on the XU pipe).
+__device__ __forceinline__ float opaque(float v) {
+  float r;
+  asm volatile("mov.b32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 // ---- Philox4x32-10 ---------------------------------------------------------------------------
 // The 10 round keys (k0 + r·0x9E3779B9, k1 + r·0xBB67AE85) are the same for every sample, so
 // the host precomputes them into the kernel parameters: the XOR reads them straight from the
@@ -56,13 +64,22 @@ inline void make_round_keys(uint64_t seed, RoundKeys* rk) {
   }
 }
 
+// 32×32→64 multiply as one IMAD.WIDE.U32 (4 FMA-heavy cycles per warp); left to itself ptxas
+// sometimes splits it into IMAD + IMAD.HI (2 + 4 cycles).
+__device__ __forceinline__ void mul_wide(uint32_t a, uint32_t m, uint32_t& hi, uint32_t& lo) {
+  asm("{\n\t.reg .u64 t;\n\tmul.wide.u32 t, %2, %3;\n\tmov.b64 {%0, %1}, t;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(a), "r"(m));
+}
+
 __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                                const RoundKeys& rk) {
   constexpr uint32_t kMul0 = 0xD2511F53u, kMul1 = 0xCD9E8D57u;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(kMul0, c0), lo0 = kMul0 * c0;
-    const uint32_t hi1 = __umulhi(kMul1, c2), lo1 = kMul1 * c2;
+    uint32_t hi0, lo0, hi1, lo1;
+    mul_wide(c0, kMul0, hi0, lo0);
+    mul_wide(c2, kMul1, hi1, lo1);
     const uint32_t n0 = hi1 ^ c1 ^ rk.k0[r];
     const uint32_t n2 = hi0 ^ c3 ^ rk.k1[r];
     c0 = n0;
@@ -106,58 +123,44 @@ __device__ __forceinline__ uint32_t ctr_word1(uint32_t b, uint32_t kw, uint32_t 
   return b | (kw << 8) | (jw << 16);
 }
 
-// ẑ of quads B.. of a sample from their Philox words (compile-time recursion over quads).
-template <int NDIM, int B = 0>
-__device__ __forceinline__ void normals_from_words(float (&z)[NDIM],
-                                                   const uint4 (&w)[(NDIM + 3) / 4]) {
-  constexpr int d = 4 * B;
-  float t0, t1, t2, t3;
-  box_muller_hat<(d + 1 < NDIM)>(w[B].x, w[B].y, t0, t1);
-  z[d] = t0;
-  if constexpr (d + 1 < NDIM) z[d + 1] = t1;
-  if constexpr (d + 2 < NDIM) {
-    box_muller_hat<(d + 3 < NDIM)>(w[B].z, w[B].w, t2, t3);
-    z[d + 2] = t2;
-    if constexpr (d + 3 < NDIM) z[d + 3] = t3;
-  }
-  if constexpr (B + 1 < (NDIM + 3) / 4) normals_from_words<NDIM, B + 1>(z, w);
-}
-
-// ẑ of one quad from its Philox words (the first min(NDIM, 4) coordinates).
+// ---- draw layout (R19) -----------------------------------------------------------------------
+// G = 4/gcd(n,4) consecutive draws share one flat stream of G·n normals (Q = G·n/4 Philox
+// blocks) when G·n ≤ 16; otherwise G = 1 and a draw owns Q = ceil(n/4) blocks. Block b of
+// draw group g has counter (g, b | kw<<8 | jw<<16, qid, tag): for n = 2, 3, 6 no normal of a
+// Philox call is wasted, and since c0 = g is common to the group's blocks while c1 differs only
+// by the compile-time b, the first Philox rounds are shared across them (their multiplies are
+// per group or warp-uniform).
 template <int NDIM>
-__device__ __forceinline__ void quad_normals_hat(float (&z)[NDIM], uint4 w) {
-  float t0, t1, t2, t3;
-  box_muller_hat<(NDIM >= 2)>(w.x, w.y, t0, t1);
-  z[0] = t0;
-  if constexpr (NDIM >= 2) z[1] = t1;
-  if constexpr (NDIM >= 3) {
-    box_muller_hat<(NDIM >= 4)>(w.z, w.w, t2, t3);
-    z[2] = t2;
-    if constexpr (NDIM >= 4) z[3] = t3;
-  }
-}
+struct DrawLayout {
+  static constexpr int G0 = (NDIM % 4 == 0) ? 1 : ((NDIM % 2 == 0) ? 2 : 4);
+  static constexpr int G = (G0 * NDIM <= 16) ? G0 : 1;
+  static constexpr int Q = (G == 1) ? (NDIM + 3) / 4 : G * NDIM / 4;
+  static constexpr int L = G * NDIM;  // normals produced per group
+};
 
-// ẑ (= z / C) of draw `draw` (= sample index, or index >> 1 under antithetic sampling).
+// The G·n normals ẑ of draw group g (sample r of the group: zz[r·n .. r·n + n − 1]).
 template <int NDIM>
-__device__ __forceinline__ void sample_normals_hat(float (&z)[NDIM], uint32_t draw, uint32_t w1base,
-                                                   uint32_t qid, uint32_t tag, const RoundKeys& rk) {
-  constexpr int kQuads = (NDIM + 3) / 4;
+__device__ __forceinline__ void group_normals_hat(float (&zz)[DrawLayout<NDIM>::L], uint32_t g,
+                                                  uint32_t w1base, uint32_t qid, uint32_t tag,
+                                                  const RoundKeys& rk) {
+  using L = DrawLayout<NDIM>;
 #pragma unroll
-  for (int b = 0; b < kQuads; ++b) {
-    const uint4 w = philox4x32_10(draw, w1base | (uint32_t)b, qid, tag, rk);
+  for (int b = 0; b < L::Q; ++b) {
+    const uint4 w = philox4x32_10(g, w1base | (uint32_t)b, qid, tag, rk);
+    constexpr int kLen = L::L;
+    const int e = 4 * b;
     float t0, t1, t2, t3;
-    box_muller_hat<true>(w.x, w.y, t0, t1);
-    if (4 * b + 0 < NDIM) z[4 * b + 0] = t0;
-    if (4 * b + 1 < NDIM) z[4 * b + 1] = t1;
-    if (4 * b + 2 < NDIM) {
-      if (4 * b + 3 < NDIM) {
-        box_muller_hat<true>(w.z, w.w, t2, t3);
-        z[4 * b + 2] = t2;
-        z[4 * b + 3] = t3;
-      } else {
-        box_muller_hat<false>(w.z, w.w, t2, t3);
-        z[4 * b + 2] = t2;
-      }
+    if (e < kLen) {
+      if (e + 1 < kLen) box_muller_hat<true>(w.x, w.y, t0, t1);
+      else box_muller_hat<false>(w.x, w.y, t0, t1);
+      zz[e] = t0;
+      if (e + 1 < kLen) zz[e + 1] = t1;
+    }
+    if (e + 2 < kLen) {
+      if (e + 3 < kLen) box_muller_hat<true>(w.z, w.w, t2, t3);
+      else box_muller_hat<false>(w.z, w.w, t2, t3);
+      zz[e + 2] = t2;
+      if (e + 3 < kLen) zz[e + 3] = t3;
     }
   }
 }

@@ -19,9 +19,6 @@
 
 namespace hjmc {
 
-#ifndef HJMC_SWP
-#define HJMC_SWP 0
-#endif
 #ifndef HJMC_UNROLL
 #define HJMC_UNROLL 2
 #endif
@@ -45,141 +42,67 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 // Accumulate the weighted sums of one Φ pass over this thread's samples.
-//   S += w,  Mz[d] += w z_d,  w = 2^(A core(y) + B)
+//   S += w,  Mz[d] += w ẑ_d,  w = 2^(A core(y) + B)
+// Samples are walked in draw groups (R19, DrawLayout): a thread generates the group's normal
+// stream (Q Philox blocks) and then runs its G samples; groups are strided over the CTA.
+template <class Tgt, int NDIM>
+__device__ __forceinline__ void accumulate_sample(const Tgt& tgt, const float (&xs)[NDIM],
+                                                  float sigma, float A, float B,
+                                                  const float* zg, float sgn, float& S,
+                                                  float (&Mz)[NDIM]) {
+  float z[NDIM];
+#pragma unroll
+  for (int d = 0; d < NDIM; ++d) z[d] = zg[d];
+  const float w = ex2_approx(fmaf(A, tgt.core(xs, sgn * sigma, z), B));
+  S += w;
+  const float sw = sgn * w;
+#pragma unroll
+  for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(sw, z[d], Mz[d]);
+}
+
 template <class Tgt, int NDIM, int NT>
-__device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[NDIM], float sigma,
-                                              float A, float B, uint32_t N, int antithetic,
-                                              uint32_t w1base, uint32_t qid, uint32_t tag, const RoundKeys& rk,
-                                              float& S, float (&Mz)[NDIM]) {
+__device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[NDIM],
+                                                   float sigma, float A, float B, uint32_t N,
+                                                   int antithetic, uint32_t w1base, uint32_t qid,
+                                                   uint32_t tag, const RoundKeys& rk, float& S,
+                                                   float (&Mz)[NDIM]) {
+  using L = DrawLayout<NDIM>;
   S = 0.f;
 #pragma unroll
   for (int d = 0; d < NDIM; ++d) Mz[d] = 0.f;
+  const uint32_t draws = antithetic ? (N >> 1) + (N & 1u) : N;
+  const uint32_t groups = (draws + L::G - 1) / L::G;
   if (!antithetic) {
-    if constexpr (HJMC_SWP && NDIM <= 4) {
-    // Software-pipelined: the Philox words of the next sample (integer multiply + logic pipes)
-    // are produced while this sample's Box–Muller, target and moments (MUFU + FP32 pipes) run.
-    uint32_t i = threadIdx.x;
-    uint4 w = philox4x32_10(i, w1base, qid, tag, rk);
-    for (; i < N; i += NT) {
-      const uint4 wc = w;
-      if (i + NT < N) w = philox4x32_10(i + NT, w1base, qid, tag, rk);
-      float z[NDIM];
-      quad_normals_hat<NDIM>(z, wc);
-      const float wt = ex2_approx(fmaf(A, tgt.core(xs, sigma, z), B));
-      S += wt;
+    const uint32_t full = N / L::G;  // groups whose G samples all exist: no per-sample guard
+#pragma unroll(L::G == 1 ? kSampleUnroll : 1)
+    for (uint32_t g = threadIdx.x; g < full; g += NT) {
+      float zz[L::L];
+      group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
 #pragma unroll
-      for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(wt, z[d], Mz[d]);
+      for (int r = 0; r < L::G; ++r)
+        accumulate_sample<Tgt, NDIM>(tgt, xs, sigma, A, B, zz + r * NDIM, 1.f, S, Mz);
     }
-    } else {
-#pragma unroll kSampleUnroll
-    for (uint32_t i = threadIdx.x; i < N; i += NT) {
-      float z[NDIM];
-      sample_normals_hat<NDIM>(z, i, w1base, qid, tag, rk);
-      const float w = ex2_approx(fmaf(A, tgt.core(xs, sigma, z), B));
-      S += w;
+    for (uint32_t g = full + threadIdx.x; g < groups; g += NT) {  // ragged tail group
+      float zz[L::L];
+      group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
 #pragma unroll
-      for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(w, z[d], Mz[d]);
-    }
+      for (int r = 0; r < L::G; ++r)
+        if (g * L::G + r < N)
+          accumulate_sample<Tgt, NDIM>(tgt, xs, sigma, A, B, zz + r * NDIM, 1.f, S, Mz);
     }
   } else {
-    const uint32_t draws = (N >> 1) + (N & 1u);
-    for (uint32_t q = threadIdx.x; q < draws; q += NT) {
-      float z[NDIM];
-      sample_normals_hat<NDIM>(z, q, w1base, qid, tag, rk);
-      const float wp = ex2_approx(fmaf(A, tgt.core(xs, sigma, z), B));
-      const float wm = (2 * q + 1 < N) ? ex2_approx(fmaf(A, tgt.core(xs, -sigma, z), B)) : 0.f;
-      S += wp + wm;
-      const float dw = wp - wm;
+    for (uint32_t g = threadIdx.x; g < groups; g += NT) {
+      float zz[L::L];
+      group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
 #pragma unroll
-      for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(dw, z[d], Mz[d]);
-    }
-  }
-}
-
-#ifndef HJMC_WS
-#define HJMC_WS 0
-#endif
-#ifndef HJMC_WS_STAGES
-#define HJMC_WS_STAGES 4
-#endif
-#ifndef HJMC_WS_SPT
-#define HJMC_WS_SPT 2
-#endif
-constexpr int kWsStages = HJMC_WS_STAGES;   // ring depth
-constexpr int kWsSpt = HJMC_WS_SPT;         // samples per thread per stage
-
-__device__ __forceinline__ void named_bar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void named_bar_arrive(int id, int count) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-// Warp-specialised Φ pass (non-antithetic): warps 0..NT/64−1 produce the Philox words of each
-// stage's samples into a shared-memory ring (integer-multiply + logic pipes); the other half
-// consume them (Box–Muller on MUFU + FP32, target, weight, moments). Each SMSP hosts one
-// producer and one consumer warp per CTA, so both pipe groups stay busy whatever phase the
-// warps are in. Stage t ↔ samples t·B .. t·B + B − 1 (B = kWsSpt·NT/2); FULL(s)/EMPTY(s) are
-// named barriers 1..2·kWsStages over all NT threads (producers arrive/sync, consumers sync/
-// arrive). Consumers skip EMPTY for the last kWsStages stages, which no producer waits for,
-// so every barrier instance is balanced at the end of the pass.
-template <int NDIM>
-struct WsRing {
-  static constexpr int kQuads = (NDIM + 3) / 4;
-  uint4 w[kWsStages][kWsSpt][128][kQuads];
-};
-
-template <class Tgt, int NDIM, int NT>
-__device__ __forceinline__ void mc_accumulate_ws(WsRing<NDIM>& ring, const Tgt& tgt,
-                                                 const float (&xs)[NDIM], float sigma, float A,
-                                                 float B, uint32_t N, uint32_t w1base,
-                                                 uint32_t qid, uint32_t tag, const RoundKeys& rk,
-                                                 float& S, float (&Mz)[NDIM]) {
-  static_assert(NT == 256, "ring layout assumes 128 producers + 128 consumers");
-  constexpr int kHalf = NT / 2;
-  constexpr int kStage = kWsSpt * kHalf;
-  constexpr int kQuads = WsRing<NDIM>::kQuads;
-  S = 0.f;
-#pragma unroll
-  for (int d = 0; d < NDIM; ++d) Mz[d] = 0.f;
-  const uint32_t stages = (N + kStage - 1) / kStage;
-  const bool producer = threadIdx.x < kHalf;
-  const int t0 = producer ? threadIdx.x : threadIdx.x - kHalf;
-  if (producer) {
-    for (uint32_t t = 0; t < stages; ++t) {
-      const int st = (int)(t % kWsStages);
-      if (t >= kWsStages) named_bar_sync(1 + kWsStages + st, NT);  // EMPTY(st)
-#pragma unroll
-      for (int e = 0; e < kWsSpt; ++e) {
-        const uint32_t i = t * kStage + e * kHalf + t0;
-        if (i < N) {
-#pragma unroll
-          for (int b = 0; b < kQuads; ++b)
-            ring.w[st][e][t0][b] = philox4x32_10(i, w1base | (uint32_t)b, qid, tag, rk);
+      for (int r = 0; r < L::G; ++r) {
+        const uint32_t q = g * L::G + r;
+        if (L::G == 1 || q < draws) {
+          accumulate_sample<Tgt, NDIM>(tgt, xs, sigma, A, B, zz + r * NDIM, 1.f, S, Mz);
+          if (2 * q + 1 < N)
+            accumulate_sample<Tgt, NDIM>(tgt, xs, sigma, A, B, zz + r * NDIM, -1.f, S, Mz);
         }
       }
-      named_bar_arrive(1 + st, NT);                                   // FULL(st)
-    }
-  } else {
-    for (uint32_t t = 0; t < stages; ++t) {
-      const int st = (int)(t % kWsStages);
-      named_bar_sync(1 + st, NT);                                     // FULL(st)
-#pragma unroll
-      for (int e = 0; e < kWsSpt; ++e) {
-        const uint32_t i = t * kStage + e * kHalf + t0;
-        if (i < N) {
-          uint4 wq[kQuads];
-#pragma unroll
-          for (int b = 0; b < kQuads; ++b) wq[b] = ring.w[st][e][t0][b];
-          float z[NDIM];
-          normals_from_words<NDIM>(z, wq);
-          const float wt = ex2_approx(fmaf(A, tgt.core(xs, sigma, z), B));
-          S += wt;
-#pragma unroll
-          for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(wt, z[d], Mz[d]);
-        }
-      }
-      if (t + kWsStages < stages) named_bar_arrive(1 + kWsStages + st, NT);  // EMPTY(st)
     }
   }
 }
@@ -189,20 +112,22 @@ template <class Tgt, int NDIM, int NT>
 __device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float sigma, float A,
                                  uint32_t N, int antithetic, uint32_t w1base, uint32_t qid,
                                  uint32_t tag, const RoundKeys& rk) {
+  using L = DrawLayout<NDIM>;
   float amax = -3.0e38f;
-  if (!antithetic) {
-    for (uint32_t i = threadIdx.x; i < N; i += NT) {
+  const uint32_t draws = antithetic ? (N >> 1) + (N & 1u) : N;
+  const uint32_t groups = (draws + L::G - 1) / L::G;
+  for (uint32_t g = threadIdx.x; g < groups; g += NT) {
+    float zz[L::L];
+    group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
+#pragma unroll
+    for (int r = 0; r < L::G; ++r) {
+      const uint32_t q = g * L::G + r;
+      if (q >= draws) continue;
       float z[NDIM];
-      sample_normals_hat<NDIM>(z, i, w1base, qid, tag, rk);
+#pragma unroll
+      for (int d = 0; d < NDIM; ++d) z[d] = zz[r * NDIM + d];
       amax = fmaxf(amax, A * tgt.core(xs, sigma, z));
-    }
-  } else {
-    const uint32_t draws = (N >> 1) + (N & 1u);
-    for (uint32_t q = threadIdx.x; q < draws; q += NT) {
-      float z[NDIM];
-      sample_normals_hat<NDIM>(z, q, w1base, qid, tag, rk);
-      amax = fmaxf(amax, A * tgt.core(xs, sigma, z));
-      if (2 * q + 1 < N) amax = fmaxf(amax, A * tgt.core(xs, -sigma, z));
+      if (antithetic && 2 * q + 1 < N) amax = fmaxf(amax, A * tgt.core(xs, -sigma, z));
     }
   }
   return amax;
@@ -354,7 +279,6 @@ constexpr int min_blocks() {
 template <class Tgt, int NDIM, int NT>
 __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __grid_constant__ SolveParams P) {
   __shared__ SolveSmem<NDIM, NT> sm;
-  __shared__ WsRing<(HJMC_WS && NDIM <= 8) ? NDIM : 1> ring;
   const int64_t unit = blockIdx.x;
   int64_t m;
   int j;
@@ -375,7 +299,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __g
   const double tau = (P.mode != kModeValueGrad) ? (double)j * P.T / (double)P.K : P.tau_vg;
   const double sigma_d = sqrt(P.gp.delta_eff * tau);
   const float sigma = (float)sigma_d;
-  const float sigma_s = (float)(sigma_d * (double)kBMScale);  // y = x + σ z = x + (σC) ẑ
+  const float sigma_s = opaque((float)(sigma_d * (double)kBMScale));  // y = x + σz = x + (σC)ẑ
   float xs[NDIM];
 #pragma unroll
   for (int d = 0; d < NDIM; ++d) {
@@ -408,21 +332,12 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __g
                         : (P.mode == kModePass) ? (P.crn ? 0u : (uint32_t)P.kiter)
                                                 : P.ktag;
     const uint32_t w1base = (kw << 8) | (jw << 16);
-    const float A = (float)(-c * kLog2e);
-    float B = -A * lowc;  // every a_i = A core_i + B ≤ 0: no weight can overflow
+    const float A = opaque((float)(-c * kLog2e));
+    float B = opaque(-A * lowc);  // every a_i = A core_i + B ≤ 0: no weight can overflow
 
     float S, Mz[NDIM];
-    if constexpr (HJMC_WS && NT == 256 && NDIM <= 8) {
-      if (!P.antithetic)
-        mc_accumulate_ws<Tgt, NDIM, NT>(ring, tgt, xs, sigma_s, A, B, P.N, w1base, id, P.tag,
-                                        P.rk, S, Mz);
-      else
-        mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id,
-                                     P.tag, P.rk, S, Mz);
-    } else {
-      mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id, P.tag,
-                                   P.rk, S, Mz);
-    }
+    mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id, P.tag,
+                                 P.rk, S, Mz);
     cta_reduce<NDIM, NT>(sm, S, Mz);
     if (!(sm.sum[0] >= (double)kUnderflowS)) {
       // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with

@@ -3,12 +3,10 @@
 The path is bound by plain ALU/MUFU arithmetic (no contraction, ~0 HBM traffic),
 so its roofline is a pipe roofline. Per eval the METHOD needs (independent of how the kernel
 is written; DESIGN.md §6 derives each line):
-  * Philox4x32-10, one call per 4 normals: 10 rounds × (2 wide multiplies + 2 three-input XORs);
-    in the first two rounds counter words 1–3 are the same for every sample, leaving
-    18 multiplies and 19 XORs per call that depend on the sample index;
-  * uniform mapping: one AND/OR + one add per 32-bit word used;
-  * Box–Muller: per radius word LG2 + SQRT + 1 multiply; per angle word 1 multiply, COS (+ SIN
-    when the second normal of the pair is used) and 1 multiply per normal produced;
+  * Philox4x32-10, one call per 4 normals (draw layout R19 wastes none for n = 2, 3, 6):
+    10 rounds × (2 wide multiplies + 2 three-input XORs); in the first two rounds counter
+    words 1–3 are the same for every sample, leaving 18 multiplies and 19 XORs per call;
+  * Box–Muller per pair: 2 mantissa builds, 1 add, LG2 + SQRT + COS + SIN, 2 multiplies;
   * y = x + σ z on the coordinates g reads, g itself, a = A·core + B (1 FFMA), 1 EX2;
   * the moment update: 1 add + n FFMAs.
 Pipe rates (lane-ops per clock per SM) default to the nominal sm_100 figures and are replaced
@@ -27,16 +25,28 @@ F_MAX_MHZ = 1965.0
 # (IMAD on the FMA-heavy half) 64; logic/ALU 64; MUFU (XU) 16
 NOMINAL_RATES = {"issue": 128.0, "fp32": 128.0, "imul": 64.0, "alu": 64.0, "mufu": 16.0}
 
+def draw_layout(n: int) -> tuple[int, int]:
+    """(G, Q): draws per group and Philox blocks per group (R19, include/hjmc.h)."""
+    g0 = 1 if n % 4 == 0 else (2 if n % 2 == 0 else 4)
+    G = g0 if g0 * n <= 16 else 1
+    Q = (n + 3) // 4 if G == 1 else G * n // 4
+    return G, Q
+
+
 def op_counts(n: int, target: str, antithetic: bool = False) -> dict:
     """Minimal lane-operation counts per eval, by pipe class (antithetic: one draw of n
-    normals serves two samples, so the draw costs are halved)."""
-    quads = (n + 3) // 4
-    pairs_used = (n + 1) // 2               # Box–Muller pairs with ≥1 normal used
-    sins = n // 2                           # second normal of a pair used
-    words = 2 * pairs_used
-    # ---- per draw: Philox + uniform mapping + Box–Muller
-    draw = {"imul": 18 * quads, "alu": 19 * quads + words + 1,
-            "fp32": words + 2 * pairs_used + n, "mufu": 3 * pairs_used + sins}
+    normals serves two samples, so the draw costs are halved).
+
+    Per draw (grouped layout): Q/G Philox calls of 18 sample-dependent wide multiplies and 19
+    XORs; per Box–Muller pair 2 mantissa builds (ALU), u = F − (1 − 2⁻²⁴) and r̂·cos, r̂·sin
+    (3 FP32), LG2 + SQRT + COS + SIN (4 MUFU; the angle a is already in revolutions, the MUFU
+    unit's native unit); a pair whose second normal is unused drops its SIN and one multiply."""
+    G, Q = draw_layout(n)
+    used = G * n                                # normals used per group
+    pairs = (used + 1) // 2
+    half = used % 2                             # a last pair with only its cos used
+    draw = {"imul": 18 * Q / G, "alu": (19 * Q + 2 * pairs) / G + 1,
+            "fp32": (3 * pairs - half) / G, "mufu": (4 * pairs - half) / G}
     # ---- per sample: y, g, weight, moments
     samp = {"imul": 0, "alu": 0, "fp32": 0, "mufu": 1}   # EX2
     if target == "quad_bowl":
@@ -47,6 +57,11 @@ def op_counts(n: int, target: str, antithetic: bool = False) -> dict:
         K = n // 3
         samp["fp32"] += 4 * K
         samp["alu"] += K
+        samp["mufu"] += 1
+    elif target == "pursuit_min":
+        A = n // 3
+        samp["fp32"] += 2 + 6 * (A - 1)
+        samp["alu"] += A - 1
         samp["mufu"] += 1
     elif target == "disk":
         samp["fp32"] += 4

@@ -204,7 +204,7 @@ class Solver:
         t = self.torch
         n = self.cfg.n
         z = t.empty((count, n), device=self.device)
-        r = t.empty((count, 4 * ((n + 3) // 4)), dtype=t.int32, device=self.device) if raw else None
+        r = t.zeros((count, 4 * ((n + 3) // 4 + 1)), dtype=t.int32, device=self.device) if raw else None
         self._check(self.L.hjmc_debug_normals(self.h, qid, jw, kw, i0, count, _ptr(z), _ptr(r),
                                               self._stream()))
         return (z, r) if raw else z

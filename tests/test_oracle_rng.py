@@ -65,14 +65,19 @@ def test_normal_bound(oracle_mod):
     assert np.abs(z).max() <= math.sqrt(48 * math.log(2)) + 1e-12
 
 
-def test_odd_dimension_uses_first_coordinates(oracle_mod):
-    z3 = _draws(oracle_mod, n=3, count=100)
-    z4 = _draws(oracle_mod, n=4, count=100)
-    np.testing.assert_array_equal(z3, z4[:, :3])
-    z6 = _draws(oracle_mod, n=6, count=100)
-    z8 = _draws(oracle_mod, n=8, count=100)
-    np.testing.assert_array_equal(z6, z8[:, :6])
-    np.testing.assert_array_equal(z6[:, :4], z4)       # quad 0 identical for any n
+def test_flat_stream_grouping(oracle_mod):
+    """R19: for G·n ≤ 16 the G = 4/gcd(n,4) draws of group γ read one flat stream from the
+    blocks (γ, b = 0..Q−1) — the same blocks a single draw of the G·n-dimensional layout uses;
+    larger n (G = 1) take ceil(n/4) blocks per draw, so n = 5 is the first 5 normals of n = 8."""
+    z4 = _draws(oracle_mod, n=4, count=20)
+    z12 = _draws(oracle_mod, n=12, count=20)
+    for n, G, ref in ((2, 2, z4), (3, 4, z12), (6, 2, z12)):
+        zn = _draws(oracle_mod, n=n, count=G * 20)
+        np.testing.assert_array_equal(zn.reshape(20, G * n), ref)
+    z8 = _draws(oracle_mod, n=8, count=30)
+    z5 = _draws(oracle_mod, n=5, count=30)
+    np.testing.assert_array_equal(z5, z8[:, :5])
+    np.testing.assert_array_equal(z8[:, :4], _draws(oracle_mod, n=4, count=30))
 
 
 def test_antithetic_pairs_exact(oracle_mod):
