@@ -77,3 +77,73 @@ def assert_c_history(O, P, x, chist_gpu, ref):
             worst = int(np.argmax(r))
             assert r.max() <= 1.0, (f"chist[{j},{k}] worst query {worst} ratio {r.max():.3g} "
                                     f"gpu={chist_gpu[j, k][worst]!r} ref={ref['chist'][j, k][worst]!r}")
+
+
+# Picard iterates in the non-contractive regime. Theorem 2 guarantees contraction
+# only when q < 1; where H(x, Dv) ≈ 0 and c is unclamped (R8) the map c ↦ Γ(x, Dv(Φ(c))) can be
+# expansive, and ANY rounding difference between two implementations grows geometrically with
+# k. There the allowed deviation at iterate k is the first-order propagation, along the
+# oracle's own trajectory, of a relative Dv perturbation ε = 1e-4 per iterate:
+#   Δc⁽⁰⁾ = ‖∇_pΓ(x, Dg)‖·ε‖Dg‖,
+#   Δv⁽ᵏ⁾ = 2e-4·max(|v|, floor) + |∂v/∂c|·Δc⁽ᵏ⁾,   ΔDv⁽ᵏ⁾ = ε‖Dv‖ + ‖∂Dv/∂c‖·Δc⁽ᵏ⁾,
+#   Δc⁽ᵏ⁺¹⁾ = 2e-4·|c⁽ᵏ⁺¹⁾| + ‖∇_pΓ(x, Dv⁽ᵏ⁾)‖·ΔDv⁽ᵏ⁾,
+# with ∂Φ/∂c from central differences of the oracle's Φ at its own c (oracle-only data).
+# Contractive queries never reach this path: their plain R20 check passes.
+def propagated_bounds(O, P, x, qid, j, c_ref, v_ref, dv_ref, floor):
+    """Allowed |Δv|, |Δc| and ‖ΔDv‖ per iterate k for one query and horizon j (1-based)."""
+    x = np.asarray(x, dtype=np.float64)
+    tau = j * P.T / P.K
+    p0 = O.dg(P, x)
+    dc = O.gamma_sensitivity(P, x, p0) * C_DV_EPS * max(np.linalg.norm(p0), P.m0)
+    bv, bc, bd = np.zeros(P.Kp), np.zeros(P.Kp), np.zeros(P.Kp)
+    for k in range(P.Kp):
+        c = float(c_ref[k])
+        bc[k] = V_RTOL * abs(c) + dc
+        h = 1e-4 * c
+        kw = 0 if P.crn else k
+        vp, dvp, _, _ = O.phi(P, x, c + h, tau, qid=int(qid), jw=j, kw=kw)
+        vm, dvm, _, _ = O.phi(P, x, c - h, tau, qid=int(qid), jw=j, kw=kw)
+        dv_dc = abs(vp - vm) / (2 * h)
+        ddv_dc = np.linalg.norm(dvp - dvm) / (2 * h)
+        bv[k] = V_RTOL * max(abs(float(v_ref[k])), floor) + dv_dc * dc
+        bdv = C_DV_EPS * np.linalg.norm(dv_ref[k]) + ddv_dc * dc
+        bd[k] = max(bdv, DV_RTOL * np.linalg.norm(dv_ref[k]))
+        if k + 1 < P.Kp:
+            dc = V_RTOL * abs(float(c_ref[k + 1])) + O.gamma_sensitivity(P, x, dv_ref[k]) * bdv
+    return bv, bc, bd
+
+
+def assert_picard_history(O, P, x, qids, vhist_gpu, chist_gpu, ref):
+    """vhist and chist at every (j, k): the plain R20 / R25 checks, and for a (query, horizon)
+    that fails them, the propagated non-contractive bound above. Returns the number of
+    (query, horizon) pairs that needed the propagated bound."""
+    x = np.asarray(x, dtype=np.float64)
+    M = x.shape[0]
+    floor = FLOOR * np.abs(ref["vhist"]).max()
+    dg = np.stack([O.dg(P, xm) for xm in x])
+    needed = 0
+    for m in range(M):
+        for j in range(P.K):
+            base_ok = True
+            for k in range(P.Kp):
+                vr = ref["vhist"][j, k, m]
+                if abs(vhist_gpu[j, k, m] - vr) > V_RTOL * max(abs(vr), floor):
+                    base_ok = False
+                    break
+                p_ref = dg[m] if k == 0 else ref["dvhist"][j, k - 1, m]
+                if c_violations(O, P, x[m:m + 1], [chist_gpu[j, k, m]], [ref["chist"][j, k, m]],
+                                p_ref[None])[0] > 1.0:
+                    base_ok = False
+                    break
+            if base_ok:
+                continue
+            needed += 1
+            bv, bc, _ = propagated_bounds(O, P, x[m], qids[m], j + 1, ref["chist"][j, :, m],
+                                       ref["vhist"][j, :, m], ref["dvhist"][j, :, m], floor)
+            for k in range(P.Kp):
+                dv = abs(vhist_gpu[j, k, m] - ref["vhist"][j, k, m])
+                dc = abs(chist_gpu[j, k, m] - ref["chist"][j, k, m])
+                assert dv <= bv[k] and dc <= bc[k], (
+                    f"query {qids[m]} horizon {j} iterate {k}: |Δv| {dv:.3g} (bound {bv[k]:.3g}), "
+                    f"|Δc| {dc:.3g} (bound {bc[k]:.3g})")
+    return needed
