@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "hjmc_kernels.cuh"
 
@@ -164,6 +165,102 @@ __device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, flo
   __syncthreads();
 }
 
+// ---- lane-group layout for the K-pair union at n = 39..48 (C5: n = 45) -----------------------
+// One sample is spread over 4 consecutive lanes; lane ℓ owns coordinates [12ℓ, 12ℓ + 12): its
+// Philox blocks b = 3ℓ..3ℓ+2 (12 = lcm(3, 4), so neither a block nor a (x, y) pair straddles
+// lanes), its pairs' partial min of |pos|², and its 12 moment accumulators. Two shuffles give
+// the group min, every lane forms the same weight, lane ℓ = 0's S is the one reduced. A lane
+// keeps 12 + 12 + 12 live floats instead of 45 + 45 + 45, so 4 CTAs fit per SM (255 → ≤ 64
+// registers). Same samples, same counters, same arithmetic as the generic path.
+template <class Tgt, int NDIM>
+struct UseLaneGroups {
+  static constexpr bool value = std::is_same<Tgt, PairUnion<NDIM>>::value && NDIM >= 37 &&
+                                NDIM <= 48;
+};
+
+template <int NDIM, int NT, bool kMaxMode>
+__device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float tau, float sigma_s,
+                                        float A, float B, uint32_t w1base, uint32_t qid,
+                                        float& S, float (&Mb)[12], float& amax) {
+  const int lane = threadIdx.x & 31, l = lane & 3;
+  const uint32_t slot = (threadIdx.x >> 5) * 8 + (lane >> 2);   // sample slot in the CTA
+  constexpr uint32_t kStride = NT / 4;
+  float xb[12];
+#pragma unroll
+  for (int c = 0; c < 12; ++c) {
+    const int d = 12 * l + c;
+    float xv = 0.f;
+    if (d < NDIM) {
+      xv = P.x[m * NDIM + d];
+      if (P.drift) xv = __fadd_rn(xv, __fmul_rn(P.drift[m * NDIM + d], tau));
+    }
+    xb[c] = xv;
+  }
+  S = 0.f;
+  amax = -3.0e38f;
+#pragma unroll
+  for (int c = 0; c < 12; ++c) Mb[c] = 0.f;
+  const uint32_t N = P.N;
+  const uint32_t iters = (N + kStride - 1) / kStride;
+  for (uint32_t t = 0; t < iters; ++t) {
+    const uint32_t i = t * kStride + slot;
+    float z[12];
+#pragma unroll
+    for (int qd = 0; qd < 3; ++qd) {
+      const uint4 w = philox4x32_10(i, w1base | (uint32_t)(3 * l + qd), qid, P.tag, P.rk);
+      box_muller_hat<true>(w.x, w.y, z[4 * qd], z[4 * qd + 1]);
+      box_muller_hat<true>(w.z, w.w, z[4 * qd + 2], z[4 * qd + 3]);
+    }
+    float best = 3.0e38f;
+#pragma unroll
+    for (int pq = 0; pq < 4; ++pq) {
+      const float a = fmaf(sigma_s, z[3 * pq], xb[3 * pq]);
+      const float b = fmaf(sigma_s, z[3 * pq + 1], xb[3 * pq + 1]);
+      const float r2 = fmaf(a, a, b * b);
+      best = (12 * l + 3 * pq + 1 < NDIM) ? fminf(best, r2) : best;
+    }
+    best = fminf(best, __shfl_xor_sync(0xffffffffu, best, 1));
+    best = fminf(best, __shfl_xor_sync(0xffffffffu, best, 2));
+    const float core = sqrt_approx(best);
+    if (i < N) {
+      if (kMaxMode) {
+        amax = fmaxf(amax, A * core);
+      } else {
+        const float wt = ex2_approx(fmaf(A, core, B));
+        S += wt;
+#pragma unroll
+        for (int c = 0; c < 12; ++c) Mb[c] = fmaf(wt, z[c], Mb[c]);
+      }
+    }
+  }
+}
+
+// Merge the lane-group sums into sm.sum (double), deterministic order.
+template <int NDIM, int NT>
+__device__ __forceinline__ void lg_reduce(SolveSmem<NDIM, NT>& sm, float S, float (&Mb)[12]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, l = lane & 3;
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {           // sum over the warp's 8 lane groups
+    S += __shfl_xor_sync(0xffffffffu, S, o);
+#pragma unroll
+    for (int c = 0; c < 12; ++c) Mb[c] += __shfl_xor_sync(0xffffffffu, Mb[c], o);
+  }
+  if (lane < 4) {
+    if (l == 0) sm.part[warp][0] = S;
+#pragma unroll
+    for (int c = 0; c < 12; ++c)
+      if (12 * l + c < NDIM) sm.part[warp][1 + 12 * l + c] = Mb[c];
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < NDIM + 1; col += NT) {
+    double acc = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) acc += (double)sm.part[w][col];
+    sm.sum[col] = acc;
+  }
+  __syncthreads();
+}
+
 // Thread 0's per-iterate epilogue (a9–a10), double precision: v and Dv from the CTA sums,
 // outputs, and the next frozen coefficient Γ(x, Dv) (returned; solve mode only).
 // Exact-stationarity skip (HJMC_FLAG_SKIP_STATIONARY, needs CRN): when Γ returns the same c,
@@ -271,13 +368,15 @@ __device__ __noinline__ double unit_prologue(const SolveParams& P, const Tgt& tg
 #ifndef HJMC_MINB
 #define HJMC_MINB 0
 #endif
-template <int NDIM>
+template <int NDIM, bool kLG>
 constexpr int min_blocks() {
-  return HJMC_MINB > 0 ? HJMC_MINB : (NDIM <= 6 ? 4 : (NDIM <= 16 ? 2 : 1));
+  return HJMC_MINB > 0 ? HJMC_MINB : ((kLG || NDIM <= 6) ? 4 : (NDIM <= 16 ? 2 : 1));
 }
 
-template <class Tgt, int NDIM, int NT>
-__global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __grid_constant__ SolveParams P) {
+// kLG: the lane-group instantiation (non-antithetic passes of UseLaneGroups targets); it does
+// not contain the generic per-thread path, so its register budget is the lane layout's.
+template <class Tgt, int NDIM, int NT, bool kLG = false>
+__global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(const __grid_constant__ SolveParams P) {
   __shared__ SolveSmem<NDIM, NT> sm;
   const int64_t unit = blockIdx.x;
   int64_t m;
@@ -335,15 +434,28 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __g
     const float A = opaque((float)(-c * kLog2e));
     float B = opaque(-A * lowc);  // every a_i = A core_i + B ≤ 0: no weight can overflow
 
-    float S, Mz[NDIM];
-    mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id, P.tag,
-                                 P.rk, S, Mz);
-    cta_reduce<NDIM, NT>(sm, S, Mz);
+    if constexpr (kLG) {
+      float S, Mb[12], amax;
+      lg_pass<NDIM, NT, false>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax);
+      lg_reduce<NDIM, NT>(sm, S, Mb);
+    } else {
+      float S, Mz[NDIM];
+      mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id, P.tag,
+                                   P.rk, S, Mz);
+      cta_reduce<NDIM, NT>(sm, S, Mz);
+    }
     if (!(sm.sum[0] >= (double)kUnderflowS)) {
       // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with
       // the exact maximum exponent, the plain two-pass log-sum-exp.
-      const float amax = warp_max(mc_max_exponent<Tgt, NDIM, NT>(
-          tgt, xs, sigma_s, A, P.N, P.antithetic, w1base, id, P.tag, P.rk));
+      float amax_t;
+      if constexpr (kLG) {
+        float S, Mb[12];
+        lg_pass<NDIM, NT, true>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax_t);
+      } else {
+        amax_t = mc_max_exponent<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, P.N, P.antithetic, w1base,
+                                                id, P.tag, P.rk);
+      }
+      const float amax = warp_max(amax_t);
       if ((threadIdx.x & 31) == 0) sm.fmax_part[threadIdx.x >> 5] = amax;
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -353,9 +465,16 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM>()) solve_kernel(const __g
       }
       __syncthreads();
       B = -sm.shift;
-      mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id, P.tag,
-                                   P.rk, S, Mz);
-      cta_reduce<NDIM, NT>(sm, S, Mz);
+      if constexpr (kLG) {
+        float S, Mb[12], am;
+        lg_pass<NDIM, NT, false>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, am);
+        lg_reduce<NDIM, NT>(sm, S, Mb);
+      } else {
+        float S, Mz[NDIM];
+        mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id,
+                                     P.tag, P.rk, S, Mz);
+        cta_reduce<NDIM, NT>(sm, S, Mz);
+      }
     }
     if (threadIdx.x == 0) {
       bool done = false;
@@ -377,7 +496,13 @@ template <class Tgt, int NDIM, int NT>
 cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
   if (units <= 0) return cudaSuccess;
   if (units > 0x7FFFFFFFLL) return cudaErrorInvalidValue;
-  solve_kernel<Tgt, NDIM, NT><<<(unsigned)units, NT, 0, s>>>(p);
+  if constexpr (UseLaneGroups<Tgt, NDIM>::value) {
+    if (!p.antithetic) {
+      solve_kernel<Tgt, NDIM, NT, true><<<(unsigned)units, NT, 0, s>>>(p);
+      return cudaGetLastError();
+    }
+  }
+  solve_kernel<Tgt, NDIM, NT, false><<<(unsigned)units, NT, 0, s>>>(p);
   return cudaGetLastError();
 }
 
