@@ -404,3 +404,59 @@ def test_brat_clamp_gpu(O):
                                np.maximum(brt["tube"].cpu().numpy(), ell), rtol=0, atol=1e-6)
     assert torch.equal(brat["v"], brt["v"])
     _compare_solve(O, s, P, x, hist_check=False)
+
+
+def test_plain_c_consumer(tmp_path):
+    """The C-ABI stands alone: a plain C program (examples/c_api_demo.c) links libhjmc.so,
+    solves through both the device and host entry points and gets identical results."""
+    import json
+    import os
+    import shutil
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    exe = str(tmp_path / "c_api_demo")
+    libdir = os.path.join(root, "paper_2605_18566_b200")
+    subprocess.run([gcc, "-O2", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "c_api_demo.c"), "-L", libdir, "-lhjmc",
+                    "-I", "/usr/local/cuda/include", "-L", "/usr/local/cuda/lib64", "-lcudart",
+                    "-Wl,-rpath," + libdir, "-lm", "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    rec = json.loads(out.stdout.strip().splitlines()[-1])
+    assert rec["identical_device_host"] and rec["M"] == 441
+    assert rec["passes"] == 2 * 441 * 4 * 3       # device + host solve, full schedule
+    assert rec["brt_points"] > 0
+
+
+def test_counter_extremes(O):
+    """Counter packing at its limits: global ids next to 2^32, horizon tag 65535, Picard tag
+    255, N not a multiple of the draw group (n = 3: G = 4) — GPU vs oracle."""
+    for n, target, params, system in ((3, "disk", (5.0,), "dubins_rel"),
+                                      (6, "rel_disk6", (1.5,), "rocket6"),
+                                      (45, "pair_union", (1.0,), "dubins_pairs")):
+        N = 1027 if n < 40 else 259
+        s, P = pair(O, n=n, delta=0.01, N=N, seed=0xFFFFFFFFFFFFFFFF, tag=0xFFFFFFFF,
+                    system=system, target=target, tgt_params=params)
+        x = I.random_queries(n, 9, -6, 6, seed=n + 100)
+        base = 0xFFFFFFFF - 8                           # ids 2^32−9 … 2^32−1
+        cc = np.full(9, 7.0, dtype=np.float32)
+        v, dv = s.value_grad(x, cc, 0.9, j_tag=65535, k_tag=255, qid_base=base)
+        vo, dvo = O.phi_batch(P, x, cc.astype(np.float64), 0.9, qid_base=base, jw=65535, kw=255)
+        assert_v(v.cpu().numpy(), vo, f"v n={n}")
+        assert_dv(dv.cpu().numpy(), dvo, f"dv n={n}")
+
+
+def test_solve_slice_lane_groups_ragged_and_antithetic(O):
+    """n = 45 pair union: the lane-group kernel with N not a multiple of its 64-sample stride,
+    and the antithetic (generic) instantiation, both against the oracle."""
+    for anti in (False, True):
+        s, P = pair(O, n=45, delta=0.01, T=1.0, K=1, Kp=2, N=333, antithetic=anti,
+                    system="dubins_pairs", target="pair_union", tgt_params=(1.0,))
+        x = np.tile(np.asarray(I.pair_fixed(15, 0.7), np.float32), (6, 1))
+        x[:, 0] = np.linspace(-3, 3, 6)
+        x[:, 1] = np.linspace(2, -2, 6)
+        _compare_solve(O, s, P, x, qid_base=11)
