@@ -42,7 +42,7 @@ class _Problem(C.Structure):
         ("m0", C.c_double), ("c_min", C.c_double), ("c_max", C.c_double), ("tag", C.c_uint32),
         ("system", C.c_int32), ("n_sys_params", C.c_int32), ("sys_params", C.c_double * 8),
         ("target", C.c_int32), ("n_tgt_params", C.c_int32), ("tgt_params", C.c_double * 72),
-        ("avoid", C.c_int32), ("avoid_params", C.c_double * 3),
+        ("avoid", C.c_int32), ("avoid_params", C.c_double * 3), ("proposal", C.c_int32),
     ]
 
 
@@ -108,6 +108,7 @@ class Problem:
     tgt_params: tuple = ()
     avoid: str = "none"
     avoid_params: tuple = ()
+    proposal: str = "plain"            # "plain" | "laplace" (R28)
 
     @classmethod
     def from_preset(cls, p, **kw):
@@ -115,7 +116,8 @@ class Problem:
                  crn=p.crn, antithetic=p.antithetic, m0=p.m0, c_min=p.c_min, c_max=p.c_max,
                  tag=p.tag, system=p.system, sys_params=tuple(p.sys_params), target=p.target,
                  tgt_params=tuple(p.tgt_params), avoid=getattr(p, "avoid", "none"),
-                 avoid_params=tuple(getattr(p, "avoid_params", ())))
+                 avoid_params=tuple(getattr(p, "avoid_params", ())),
+                 proposal=getattr(p, "proposal", "plain"))
         d.update(kw)
         return cls(**d)
 
@@ -135,6 +137,7 @@ class Problem:
         for i, v in enumerate(self.tgt_params):
             s.tgt_params[i] = v
         s.avoid = AVOIDS[self.avoid]
+        s.proposal = {"plain": 0, "laplace": 1}[self.proposal]
         for i, v in enumerate(self.avoid_params):
             s.avoid_params[i] = v
         return s

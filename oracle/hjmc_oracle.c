@@ -327,7 +327,7 @@ int orc_phi(const orc_problem* P, const double* x, const double* drift, uint32_t
             double* se_dv) {
   int n = P->n;
   uint32_t N = P->N;
-  double xs[ORC_MAX_N], z[ORC_MAX_N], y[ORC_MAX_N];
+  double xs[ORC_MAX_N], z[ORC_MAX_N], y[ORC_MAX_N], mu[ORC_MAX_N], ze[ORC_MAX_N];
   for (int d = 0; d < n; ++d) xs[d] = x[d] + (drift ? drift[d] * tau : 0.0);
   if (tau <= 0.0) { /* sigma = 0: the kernel is a point mass, v = g(x) and Dv = Dg */
     *v = orc_target_g(P, xs);
@@ -337,32 +337,49 @@ int orc_phi(const orc_problem* P, const double* x, const double* drift, uint32_t
     return isfinite(*v) ? 0 : 2;
   }
   double sigma = sqrt(delta_eff(P) * tau);
+  /* Proposal (R28). Plain: y ~ N(xs, sigma^2 I) as in Cor. logsumexp. Laplace-tilted:
+   * y ~ N(mu, sigma^2 I), mu = xs - c sigma^2 Dg(xs) (one step toward the mode of
+   * e^{-c g(y)} phi_sigma(y - xs)), each sample weighted by the likelihood ratio
+   * phi_sigma(y - xs) / phi_sigma(y - mu), so E_q[e^{-cg} LR] = E_p[e^{-cg}] (same v, Dv). */
+  if (P->proposal == 1) {
+    double dg[ORC_MAX_N];
+    orc_target_dg(P, xs, dg);
+    for (int d = 0; d < n; ++d) mu[d] = xs[d] - c * sigma * sigma * dg[d];
+  } else {
+    for (int d = 0; d < n; ++d) mu[d] = xs[d];
+  }
   double* a = (double*)malloc(sizeof(double) * (size_t)N);
   if (!a) return 1;
-  /* pass 1: exponents a_i = -c g(y_i) */
+  /* pass 1: exponents a_i = -c g(y_i) + log LR_i */
   double gmin = INFINITY, gsum = 0.0, A = -INFINITY;
   for (uint32_t i = 0; i < N; ++i) {
     orc_sample_normals(P, qid, jw, kw, i, z, NULL);
-    for (int d = 0; d < n; ++d) y[d] = xs[d] + sigma * z[d];
+    double r2x = 0.0, r2m = 0.0;
+    for (int d = 0; d < n; ++d) {
+      y[d] = mu[d] + sigma * z[d];
+      r2x += (y[d] - xs[d]) * (y[d] - xs[d]);
+      r2m += (y[d] - mu[d]) * (y[d] - mu[d]);
+    }
     double g = orc_target_g(P, y);
     if (g < gmin) gmin = g;
     gsum += g;
-    a[i] = -c * g;
+    a[i] = -c * g - (r2x - r2m) / (2.0 * sigma * sigma);
     if (a[i] > A) A = a[i];
   }
-  /* pass 2: S = sum exp(a_i - A), M = sum exp(a_i - A) z_i */
+  /* pass 2: S = sum exp(a_i - A), M = sum exp(a_i - A) (y_i - xs)/sigma */
   double S = 0.0, S2 = 0.0;
   double Mz[ORC_MAX_N], Mzz[ORC_MAX_N], Mz2[ORC_MAX_N];
   for (int d = 0; d < n; ++d) Mz[d] = Mzz[d] = Mz2[d] = 0.0;
   for (uint32_t i = 0; i < N; ++i) {
     orc_sample_normals(P, qid, jw, kw, i, z, NULL);
+    for (int d = 0; d < n; ++d) ze[d] = z[d] + (mu[d] - xs[d]) / sigma;  /* (y_i - xs)/sigma */
     double w = exp(a[i] - A);
     S += w;
     S2 += w * w;
     for (int d = 0; d < n; ++d) {
-      Mz[d] += w * z[d];
-      Mz2[d] += w * w * z[d];
-      Mzz[d] += w * w * z[d] * z[d];
+      Mz[d] += w * ze[d];
+      Mz2[d] += w * w * ze[d];
+      Mzz[d] += w * w * ze[d] * ze[d];
     }
   }
   free(a);

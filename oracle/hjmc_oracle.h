@@ -60,6 +60,7 @@ typedef struct orc_problem {
   double tgt_params[ORC_MAX_PARAMS];
   int32_t avoid;            /* BRAT obstacle: ORC_AVOID_* */
   double avoid_params[3];   /* disk: centre (x0, x1) and radius */
+  int32_t proposal;         /* 0: plain N(x, sigma^2 I); 1: Laplace-tilted (R28) */
 } orc_problem;
 
 void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

@@ -43,6 +43,7 @@ class Preset:
     tag: int = 0
     avoid: str = "none"          # BRAT obstacle: "none" | "disk"
     avoid_params: tuple = ()     # disk: (centre x0, centre x1, radius)
+    proposal: str = "plain"      # "plain" | "laplace": tilted importance proposal (R28)
     # slice layout
     grid_axes: tuple = (0, 1)    # which state coordinates vary over the 2-D grid
     grid_lo: float = -1.0

@@ -254,3 +254,52 @@ def test_target_values(oracle_mod):
     assert list(O.dg(P, (0, 0, 0, 3, 4, 0, 9, 9, 0))) == [1, 0, 0, 0, 0, 0, 0, 0, 0]  # e1 at ρ = 0
     P = O.Problem(n=2, target="quad_bowl", tgt_params=(0.25,))
     assert O.g(P, (1.0, 1.0)) == 0.75
+
+
+# ---- Laplace-tilted proposal (R28) -----------------------------------------------
+def test_tilted_linear_target_is_zero_variance(oracle_mod):
+    """g = a·y + b: μ = x − cσ²a is the exact mode, the likelihood-ratio weights are constant and
+    v̂ equals the Gaussian-tilt value a·x + b − cσ²|a|²/2 for ANY N (even N = 1)."""
+    O = oracle_mod
+    a = np.array([0.7, -1.2, 0.4])
+    for N in (1, 17, 3000):
+        P = O.Problem(n=3, N=N, target="linear", tgt_params=tuple(a) + (0.3,), proposal="laplace")
+        for c, tau in ((1.0, 0.5), (5.0, 0.1)):
+            x = np.array([0.2, -0.4, 1.1])
+            v, dv, diag, se = O.phi(P, x, c, tau)
+            s2 = P.delta_eff * tau
+            assert abs(v - (a @ x + 0.3 - c * s2 * a @ a / 2)) < 1e-12
+            assert abs(diag[2] - N) < 1e-6 * N           # ESS = N: every weight equal
+
+
+def test_tilted_quadratic_closed_form_and_ess(oracle_mod):
+    """Quadratic bowl: the tilted estimator matches the closed form within its SE
+    and, where the plain weights collapse (c|x|² large), has a far larger effective sample size."""
+    O = oracle_mod
+    c = 20.0
+    for x in ((0.0, 0.0), (1.0, 1.0), (-0.9, 0.3)):
+        Pp = O.Problem(n=2, delta=0.05, T=0.5, N=1 << 15, target="quad_bowl", tgt_params=(0.25,))
+        Pt = O.Problem(n=2, delta=0.05, T=0.5, N=1 << 15, target="quad_bowl", tgt_params=(0.25,),
+                       proposal="laplace")
+        vx, dvx = quad_bowl_closed_form(x, 0.25, c, 0.05 * 0.5)
+        vt, dvt, dt, st = O.phi(Pt, x, c, 0.5, qid=3)
+        vp, dvp, dp, sp = O.phi(Pp, x, c, 0.5, qid=3)
+        assert abs(vt - vx) < KSE * dt[3] + 1e-12
+        assert np.all(np.abs(dvt - dvx) < KSE * st + 1e-12)
+        if np.dot(x, x) > 1:
+            assert dt[2] > 3 * dp[2]                     # ESS
+            assert dt[3] < dp[3] / 2                     # SE of v
+
+
+def test_tilted_agrees_with_plain_on_games(oracle_mod):
+    """Disk (Dubins) and pair-union targets: tilted and plain estimates of the same Φ agree
+    within their combined standard errors (both estimate E_p[e^{−cg}])."""
+    O = oracle_mod
+    cases = [(3, "dubins_rel", "disk", (5.0,), (4.0, 3.5, 1.0), 20.0, 1.0),
+             (15, "dubins_pairs", "pair_union", (1.0,), tuple([1.1, 0.4, 0.0, 0.9, -0.8, 0.0] + [12.0, 0, 0] * 3), 5.0, 0.5)]
+    for n, system, target, tp, x, c, tau in cases:
+        kw = dict(n=n, delta=0.01, N=1 << 15, system=system, target=target, tgt_params=tp)
+        vp, dvp, dp, sp = O.phi(O.Problem(**kw), x, c, tau, qid=5)
+        vt, dvt, dt, st = O.phi(O.Problem(**kw, proposal="laplace"), x, c, tau, qid=5)
+        assert abs(vp - vt) < KSE * math.hypot(dp[3], dt[3])
+        assert np.all(np.abs(dvp - dvt) < KSE * np.hypot(sp, st) + 1e-9)
