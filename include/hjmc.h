@@ -153,6 +153,16 @@ extern "C" {
  * Outputs are identical with and without the flag; hjmc_pass_count() reports the work done. */
 #define HJMC_FLAG_SKIP_STATIONARY 2u
 
+/* Sampling proposal of a Φ pass (reading R28).
+ *  PLAIN:   y_i = x + bτ + σ z_i — the estimator of Cor. logsumexp / mc_gradient.
+ *  LAPLACE: y_i = μ + σ z_i with μ = x + bτ − c σ² Dg(x + bτ) (one step toward the mode of
+ *           e^{−c g(y)} φ_σ(y − x − bτ)); each sample carries the likelihood ratio
+ *           φ_σ(y − x − bτ)/φ_σ(y − μ), so v and Dv estimate the same quantities with lower
+ *           variance where the weights concentrate (c‖g‖ ≫ 1). Exactly zero-variance
+ *           for linear g. Dv = −E_W[(y − x − bτ)/σ]/(cσ). */
+#define HJMC_PROPOSAL_PLAIN 0
+#define HJMC_PROPOSAL_LAPLACE 1
+
 /* Systems (Hamiltonians). */
 #define HJMC_SYS_QUADRATIC 0
 #define HJMC_SYS_DUBINS_REL 1
@@ -195,6 +205,7 @@ typedef struct hjmc_config {
   uint32_t tag;       /* Philox counter word c3 (independent stream family)                   */
   int32_t device;     /* CUDA device ordinal                                                  */
   uint32_t flags;     /* HJMC_FLAG_*                                                          */
+  int32_t proposal;   /* HJMC_PROPOSAL_* (default PLAIN)                                      */
 } hjmc_config;
 
 /* Outputs of hjmc_solve_slice. Every pointer may be NULL (= do not write). */

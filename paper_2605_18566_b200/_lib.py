@@ -21,6 +21,7 @@ AVOIDS = {"none": 0, "disk": 1}
 VISC = {"paper": 0, "full": 1}
 FLAG_SYNC_CHECK = 1
 FLAG_SKIP_STATIONARY = 2
+PROPOSALS = {"plain": 0, "laplace": 1}
 
 EXPORTS = [
     "hjmc_config_defaults", "hjmc_create", "hjmc_destroy", "hjmc_set_dynamics", "hjmc_set_target",
@@ -37,6 +38,7 @@ class Config(C.Structure):
         ("Kp", C.c_int32), ("N", C.c_uint32), ("seed", C.c_uint64), ("visc", C.c_int32),
         ("crn", C.c_int32), ("antithetic", C.c_int32), ("m0", C.c_float), ("c_min", C.c_float),
         ("c_max", C.c_float), ("tag", C.c_uint32), ("device", C.c_int32), ("flags", C.c_uint32),
+        ("proposal", C.c_int32),
     ]
 
 

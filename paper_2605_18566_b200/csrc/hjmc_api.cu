@@ -97,6 +97,7 @@ void fill_common(const hjmc_handle* h, SolveParams* p) {
   p->tag = h->cfg.tag;
   p->crn = h->cfg.crn;
   p->antithetic = h->cfg.antithetic;
+  p->proposal = h->cfg.proposal;
   p->gp.delta_eff = delta_eff(h->cfg);
   p->gp.m0 = h->cfg.m0;
   p->gp.c_min = h->cfg.c_min;
@@ -144,6 +145,7 @@ void hjmc_config_defaults(hjmc_config* c) {
   c->tag = 0;
   c->device = 0;
   c->flags = 0;
+  c->proposal = HJMC_PROPOSAL_PLAIN;
 }
 
 int hjmc_version(void) { return HJMC_VERSION_MAJOR * 1000 + HJMC_VERSION_MINOR; }
@@ -167,6 +169,8 @@ int hjmc_create(const hjmc_config* cfg, hjmc_handle** out) {
     return fail(nullptr, HJMC_EINVAL, "visc must be 0 or 1");
   if (c.crn != 0 && c.crn != 1) return fail(nullptr, HJMC_EINVAL, "crn must be 0 or 1");
   if (c.antithetic != 0 && c.antithetic != 1) return fail(nullptr, HJMC_EINVAL, "antithetic must be 0 or 1");
+  if (c.proposal != HJMC_PROPOSAL_PLAIN && c.proposal != HJMC_PROPOSAL_LAPLACE)
+    return fail(nullptr, HJMC_EINVAL, "proposal must be PLAIN or LAPLACE");
   if (c.flags & ~(HJMC_FLAG_SYNC_CHECK | HJMC_FLAG_SKIP_STATIONARY))
     return fail(nullptr, HJMC_EINVAL, "unknown flag bits");
   int ndev = 0;

@@ -26,6 +26,7 @@ struct SolveParams {
   RoundKeys rk;            // Philox round keys of cfg.seed
   uint32_t tag;
   int crn, antithetic;
+  int proposal;            // HJMC_PROPOSAL_* (R28)
   GammaParams gp;
   SystemParams sp;
   TargetParams tp;

@@ -46,27 +46,35 @@ __device__ __forceinline__ float warp_max(float v) {
 //   S += w,  Mz[d] += w ẑ_d,  w = 2^(A core(y) + B)
 // Samples are walked in draw groups (R19, DrawLayout): a thread generates the group's normal
 // stream (Q Philox blocks) and then runs its G samples; groups are strided over the CTA.
-template <class Tgt, int NDIM>
+// kTilt (Laplace proposal, R28): the log2 weight gains the likelihood-ratio term sgn·(tz·ẑ).
+template <class Tgt, int NDIM, bool kTilt>
 __device__ __forceinline__ void accumulate_sample(const Tgt& tgt, const float (&xs)[NDIM],
                                                   float sigma, float A, float B,
-                                                  const float* zg, float sgn, float& S,
-                                                  float (&Mz)[NDIM]) {
+                                                  const float (&tz)[NDIM], const float* zg,
+                                                  float sgn, float& S, float (&Mz)[NDIM]) {
   float z[NDIM];
 #pragma unroll
   for (int d = 0; d < NDIM; ++d) z[d] = zg[d];
-  const float w = ex2_approx(fmaf(A, tgt.core(xs, sgn * sigma, z), B));
+  float a = fmaf(A, tgt.core(xs, sgn * sigma, z), B);
+  if constexpr (kTilt) {
+    float t = 0.f;
+#pragma unroll
+    for (int d = 0; d < NDIM; ++d) t = fmaf(tz[d], z[d], t);
+    a = fmaf(sgn, t, a);
+  }
+  const float w = ex2_approx(a);
   S += w;
   const float sw = sgn * w;
 #pragma unroll
   for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(sw, z[d], Mz[d]);
 }
 
-template <class Tgt, int NDIM, int NT>
+template <class Tgt, int NDIM, int NT, bool kTilt = false>
 __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[NDIM],
                                                    float sigma, float A, float B, uint32_t N,
                                                    int antithetic, uint32_t w1base, uint32_t qid,
                                                    uint32_t tag, const RoundKeys& rk, float& S,
-                                                   float (&Mz)[NDIM]) {
+                                                   float (&Mz)[NDIM], const float (&tz)[NDIM]) {
   using L = DrawLayout<NDIM>;
   S = 0.f;
 #pragma unroll
@@ -81,7 +89,7 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
       group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
 #pragma unroll
       for (int r = 0; r < L::G; ++r)
-        accumulate_sample<Tgt, NDIM>(tgt, xs, sigma, A, B, zz + r * NDIM, 1.f, S, Mz);
+        accumulate_sample<Tgt, NDIM, kTilt>(tgt, xs, sigma, A, B, tz, zz + r * NDIM, 1.f, S, Mz);
     }
     for (uint32_t g = full + threadIdx.x; g < groups; g += NT) {  // ragged tail group
       float zz[L::L];
@@ -89,7 +97,7 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
 #pragma unroll
       for (int r = 0; r < L::G; ++r)
         if (g * L::G + r < N)
-          accumulate_sample<Tgt, NDIM>(tgt, xs, sigma, A, B, zz + r * NDIM, 1.f, S, Mz);
+          accumulate_sample<Tgt, NDIM, kTilt>(tgt, xs, sigma, A, B, tz, zz + r * NDIM, 1.f, S, Mz);
     }
   } else {
     for (uint32_t g = threadIdx.x; g < groups; g += NT) {
@@ -99,9 +107,9 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
       for (int r = 0; r < L::G; ++r) {
         const uint32_t q = g * L::G + r;
         if (L::G == 1 || q < draws) {
-          accumulate_sample<Tgt, NDIM>(tgt, xs, sigma, A, B, zz + r * NDIM, 1.f, S, Mz);
+          accumulate_sample<Tgt, NDIM, kTilt>(tgt, xs, sigma, A, B, tz, zz + r * NDIM, 1.f, S, Mz);
           if (2 * q + 1 < N)
-            accumulate_sample<Tgt, NDIM>(tgt, xs, sigma, A, B, zz + r * NDIM, -1.f, S, Mz);
+            accumulate_sample<Tgt, NDIM, kTilt>(tgt, xs, sigma, A, B, tz, zz + r * NDIM, -1.f, S, Mz);
         }
       }
     }
@@ -112,7 +120,7 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
 template <class Tgt, int NDIM, int NT>
 __device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float sigma, float A,
                                  uint32_t N, int antithetic, uint32_t w1base, uint32_t qid,
-                                 uint32_t tag, const RoundKeys& rk) {
+                                 uint32_t tag, const RoundKeys& rk, const float (&tz)[NDIM]) {
   using L = DrawLayout<NDIM>;
   float amax = -3.0e38f;
   const uint32_t draws = antithetic ? (N >> 1) + (N & 1u) : N;
@@ -127,8 +135,11 @@ __device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float 
       float z[NDIM];
 #pragma unroll
       for (int d = 0; d < NDIM; ++d) z[d] = zz[r * NDIM + d];
-      amax = fmaxf(amax, A * tgt.core(xs, sigma, z));
-      if (antithetic && 2 * q + 1 < N) amax = fmaxf(amax, A * tgt.core(xs, -sigma, z));
+      float t = 0.f;  // tilt term (zero for the plain proposal)
+#pragma unroll
+      for (int d = 0; d < NDIM; ++d) t = fmaf(tz[d], z[d], t);
+      amax = fmaxf(amax, fmaf(A, tgt.core(xs, sigma, z), t));
+      if (antithetic && 2 * q + 1 < N) amax = fmaxf(amax, fmaf(A, tgt.core(xs, -sigma, z), -t));
     }
   }
   return amax;
@@ -138,6 +149,7 @@ template <int NDIM, int NT>
 struct SolveSmem {
   float part[NT / 32][NDIM + 1];
   double sum[NDIM + 1];
+  double dg[NDIM];  // Dg(x + bτ) for the Laplace proposal (R28)
   float fmax_part[NT / 32];
   double c_next;
   float shift;
@@ -266,22 +278,27 @@ __device__ __forceinline__ void lg_reduce(SolveSmem<NDIM, NT>& sm, float S, floa
 // Exact-stationarity skip (HJMC_FLAG_SKIP_STATIONARY, needs CRN): when Γ returns the same c,
 // the next pass has bit-identical inputs (same samples, same c), hence bit-identical outputs;
 // the remaining iterates are copied instead of recomputed and *done is set.
+// dshift (Laplace proposal only, else null): (μ − x)/σ of the pass; the likelihood ratio
+// contributes −|μ − x|²/(2σ²) to the log-mean and (μ − x)/σ to E_W[(y − x)/σ] (R28).
 template <class Tgt, int NDIM>
 __device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tgt, int64_t m, int j,
                                              int k, uint32_t id, double c, double sigma_d,
                                              float A, float B, float core_ref, const double* sum,
-                                             bool* done) {
+                                             const double* dshift, bool* done) {
   const double A_d = -c * kLog2e;
   const double Ssum = sum[0];
-  // log2 of (1/N) Σ exp(−c g_i): undo the shift B and the fp32 rounding of A
+  double tilt_log2 = 0.0;
+  if (dshift)
+    for (int d = 0; d < NDIM; ++d) tilt_log2 -= 0.5 * dshift[d] * dshift[d] * kLog2e;
+  // log2 of (1/N) Σ exp(−c g_i)·LR_i: undo the shift B and the fp32 rounding of A
   const double log2mean = log2(Ssum) - log2((double)P.N) - (double)B + A_d * (double)tgt.off +
-                          (A_d - (double)A) * (double)core_ref;
+                          (A_d - (double)A) * (double)core_ref + tilt_log2;
   const double v = -(kLn2 / c) * log2mean;                           // Cor. logsumexp
   double dv[NDIM];
   bool finite = isfinite(v);
   for (int d = 0; d < NDIM; ++d) {
     // Cor. mc_gradient; the sums hold ẑ = z/C (hjmc_rng.cuh), so E_w[z] = C·M̂/S
-    dv[d] = -((double)kBMScale * sum[1 + d] / Ssum) / (c * sigma_d);
+    dv[d] = -((double)kBMScale * sum[1 + d] / Ssum + (dshift ? dshift[d] : 0.0)) / (c * sigma_d);
     finite = finite && isfinite(dv[d]);
   }
   if (!finite && P.err) {
@@ -329,7 +346,8 @@ __device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tg
       if (P.v) P.v[m] = (float)v;
       if (P.dv)
         for (int d = 0; d < NDIM; ++d)
-          P.dv[m * NDIM + d] = (float)(-((double)kBMScale * sum[1 + d] / Ssum) / (c * sigma_d));
+          P.dv[m * NDIM + d] = (float)(-((double)kBMScale * sum[1 + d] / Ssum +
+                                         (dshift ? dshift[d] : 0.0)) / (c * sigma_d));
       if (P.c_out) P.c_out[m] = (float)c_next;
     }
   }
@@ -341,8 +359,12 @@ __device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tg
 // the unit is complete because σ = 0; the caller flags that case).
 template <class Tgt, int NDIM>
 __device__ __noinline__ double unit_prologue(const SolveParams& P, const Tgt& tgt, int64_t m, int j,
-                                             double sigma_d, const float* xs) {
+                                             double sigma_d, const float* xs, double* dg_out) {
   double xd[NDIM], p[NDIM];
+  if (P.proposal) {
+    for (int d = 0; d < NDIM; ++d) xd[d] = (double)xs[d];
+    tgt.dg(xd, dg_out);
+  }
   for (int d = 0; d < NDIM; ++d) xd[d] = (double)P.x[m * NDIM + d];
   if (P.mode == kModeSolve && j == 1 && P.g0) P.g0[m] = (float)tgt.g_host(xd);
   if (sigma_d == 0.0) {  // τ = 0: point mass, v = g(x), Dv = Dg(x)
@@ -407,7 +429,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
   }
 
   if (threadIdx.x == 0) {
-    sm.c_next = unit_prologue<Tgt, NDIM>(P, tgt, m, j, sigma_d, xs);
+    sm.c_next = unit_prologue<Tgt, NDIM>(P, tgt, m, j, sigma_d, xs, sm.dg);
     sm.shift = (sigma_d == 0.0) ? 1.f : 0.f;
   }
   __syncthreads();
@@ -416,14 +438,6 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
   __syncthreads();
 
   const uint32_t jw = (P.mode != kModeValueGrad) ? (uint32_t)j : P.jtag;
-  float core_ref;
-  {
-    float z0[NDIM];
-#pragma unroll
-    for (int d = 0; d < NDIM; ++d) z0[d] = 0.f;
-    core_ref = tgt.core(xs, 0.f, z0);
-  }
-  const float lowc = tgt.core_lower(xs, sigma);
   unsigned passes = 0;  // Φ passes this unit executed (thread 0)
 
   for (int k = 0; k < P.Kp; ++k) {
@@ -432,7 +446,34 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
                                                 : P.ktag;
     const uint32_t w1base = (kw << 8) | (jw << 16);
     const float A = opaque((float)(-c * kLog2e));
-    float B = opaque(-A * lowc);  // every a_i = A core_i + B ≤ 0: no weight can overflow
+    // Proposal centre (R28): plain → x + bτ; Laplace → μ = x + bτ − cσ²·Dg(x + bτ) (fp32, every
+    // thread computes the same values in double); tz = log2-domain tilt per ẑ coordinate.
+    float ctr[NDIM], tz[NDIM];
+    float tilt_max = 0.f;
+#pragma unroll
+    for (int d = 0; d < NDIM; ++d) {
+      ctr[d] = xs[d];
+      tz[d] = 0.f;
+    }
+    if (P.proposal) {
+#pragma unroll
+      for (int d = 0; d < NDIM; ++d) {
+        ctr[d] = (float)((double)xs[d] - c * sigma_d * sigma_d * sm.dg[d]);
+        const double dsh = ((double)ctr[d] - (double)xs[d]) / sigma_d;
+        tz[d] = opaque((float)(-kLog2e * (double)kBMScale * dsh));
+        tilt_max += fabsf(tz[d]);
+      }
+      tilt_max *= kZmax / kBMScale;  // |ẑ_d| ≤ kZmax / C
+    }
+    float core_ref;
+    {
+      float z0[NDIM];
+#pragma unroll
+      for (int d = 0; d < NDIM; ++d) z0[d] = 0.f;
+      core_ref = tgt.core(ctr, 0.f, z0);
+    }
+    // every a_i = A core_i + B (+ tilt) ≤ 0: no weight can overflow
+    float B = opaque(-A * tgt.core_lower(ctr, sigma) - tilt_max);
 
     if constexpr (kLG) {
       float S, Mb[12], amax;
@@ -440,8 +481,12 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
       lg_reduce<NDIM, NT>(sm, S, Mb);
     } else {
       float S, Mz[NDIM];
-      mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id, P.tag,
-                                   P.rk, S, Mz);
+      if (P.proposal)
+        mc_accumulate<Tgt, NDIM, NT, true>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base, id,
+                                           P.tag, P.rk, S, Mz, tz);
+      else
+        mc_accumulate<Tgt, NDIM, NT, false>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
+                                            id, P.tag, P.rk, S, Mz, tz);
       cta_reduce<NDIM, NT>(sm, S, Mz);
     }
     if (!(sm.sum[0] >= (double)kUnderflowS)) {
@@ -452,8 +497,8 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         float S, Mb[12];
         lg_pass<NDIM, NT, true>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax_t);
       } else {
-        amax_t = mc_max_exponent<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, P.N, P.antithetic, w1base,
-                                                id, P.tag, P.rk);
+        amax_t = mc_max_exponent<Tgt, NDIM, NT>(tgt, ctr, sigma_s, A, P.N, P.antithetic, w1base,
+                                                id, P.tag, P.rk, tz);
       }
       const float amax = warp_max(amax_t);
       if ((threadIdx.x & 31) == 0) sm.fmax_part[threadIdx.x >> 5] = amax;
@@ -471,15 +516,22 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         lg_reduce<NDIM, NT>(sm, S, Mb);
       } else {
         float S, Mz[NDIM];
-        mc_accumulate<Tgt, NDIM, NT>(tgt, xs, sigma_s, A, B, P.N, P.antithetic, w1base, id,
-                                     P.tag, P.rk, S, Mz);
+        if (P.proposal)
+          mc_accumulate<Tgt, NDIM, NT, true>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
+                                             id, P.tag, P.rk, S, Mz, tz);
+        else
+          mc_accumulate<Tgt, NDIM, NT, false>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
+                                              id, P.tag, P.rk, S, Mz, tz);
         cta_reduce<NDIM, NT>(sm, S, Mz);
       }
     }
     if (threadIdx.x == 0) {
       bool done = false;
+      double dsh[NDIM];
+      if (P.proposal)
+        for (int d = 0; d < NDIM; ++d) dsh[d] = ((double)ctr[d] - (double)xs[d]) / sigma_d;
       sm.c_next = pass_epilogue<Tgt, NDIM>(P, tgt, m, j, k, id, c, sigma_d, A, B, core_ref, sm.sum,
-                                           &done);
+                                           P.proposal ? dsh : nullptr, &done);
       sm.shift = done ? 1.f : 0.f;
       ++passes;
     }
@@ -497,7 +549,7 @@ cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
   if (units <= 0) return cudaSuccess;
   if (units > 0x7FFFFFFFLL) return cudaErrorInvalidValue;
   if constexpr (UseLaneGroups<Tgt, NDIM>::value) {
-    if (!p.antithetic) {
+    if (!p.antithetic && !p.proposal) {
       solve_kernel<Tgt, NDIM, NT, true><<<(unsigned)units, NT, 0, s>>>(p);
       return cudaGetLastError();
     }

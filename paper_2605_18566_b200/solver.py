@@ -39,13 +39,15 @@ class SolverConfig:
     tgt_params: tuple = ()
     avoid: str = "none"
     avoid_params: tuple = ()
+    proposal: str = "plain"      # "plain" | "laplace" (R28)
 
     @classmethod
     def from_preset(cls, p: Preset, **kw) -> "SolverConfig":
         d = dict(n=p.n, delta=p.delta, T=p.T, K=p.K, Kp=p.Kp, N=p.N, seed=p.seed, visc=p.visc,
                  crn=p.crn, antithetic=p.antithetic, m0=p.m0, c_min=p.c_min, c_max=p.c_max,
                  tag=p.tag, system=p.system, sys_params=tuple(p.sys_params), target=p.target,
-                 tgt_params=tuple(p.tgt_params), avoid=p.avoid, avoid_params=tuple(p.avoid_params))
+                 tgt_params=tuple(p.tgt_params), avoid=p.avoid, avoid_params=tuple(p.avoid_params),
+                 proposal=p.proposal)
         d.update(kw)
         return cls(**d)
 
@@ -56,6 +58,7 @@ class SolverConfig:
         c.visc = _lib.VISC[self.visc]
         c.crn, c.antithetic = int(self.crn), int(self.antithetic)
         c.m0, c.c_min, c.c_max, c.tag, c.device = self.m0, self.c_min, self.c_max, self.tag, self.device
+        c.proposal = _lib.PROPOSALS[self.proposal]
         c.flags = (_lib.FLAG_SYNC_CHECK if self.sync_check else 0) | (
             _lib.FLAG_SKIP_STATIONARY if self.skip_stationary else 0)
         return c

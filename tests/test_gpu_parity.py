@@ -460,3 +460,42 @@ def test_solve_slice_lane_groups_ragged_and_antithetic(O):
         x[:, 0] = np.linspace(-3, 3, 6)
         x[:, 1] = np.linspace(2, -2, 6)
         _compare_solve(O, s, P, x, qid_base=11)
+
+
+@pytest.mark.parametrize("target,n,params,system,c,tau", [
+    ("disk", 3, (5.0,), "dubins_rel", 20.0, 0.7),
+    ("quad_bowl", 2, (0.25,), "quadratic", 20.0, 0.5),
+    ("rel_disk6", 6, (1.5,), "rocket6", 12.0, 1.0),
+    ("pair_union", 45, (1.0,), "dubins_pairs", 5.0, 0.5),
+])
+def test_laplace_proposal_value_grad(O, target, n, params, system, c, tau):
+    """Laplace-tilted proposal (R28): GPU vs oracle on the same samples."""
+    N = 2049 if n < 40 else 515
+    s, P = pair(O, n=n, delta=0.01, N=N, seed=5, system=system, target=target,
+                tgt_params=params, proposal="laplace")
+    lo, hi = (-1.2, 1.2) if target == "quad_bowl" else (-7, 7)
+    x = I.random_queries(n, 23, lo, hi, seed=n + 7)
+    cc = np.full(23, c, dtype=np.float32)
+    v, dv = s.value_grad(x, cc, tau, j_tag=2, k_tag=1, qid_base=70)
+    vo, dvo = O.phi_batch(P, x, cc.astype(np.float64), tau, qid_base=70, jw=2, kw=1)
+    assert_v(v.cpu().numpy(), vo)
+    assert_dv(dv.cpu().numpy(), dvo)
+
+
+def test_laplace_proposal_zero_variance_linear():
+    """g = a·y + b: the tilted estimator is exact for any N — the GPU returns the Gaussian-tilt
+    value a·x + b − cσ²|a|²/2 to fp32 precision with N = 7."""
+    a = np.array([0.7, -1.2, 0.4])
+    s = Solver(SolverConfig(n=3, delta=0.01, N=7, target="linear", tgt_params=tuple(a) + (0.3,),
+                            proposal="laplace"))
+    x = I.random_queries(3, 64, -2, 2, seed=4)
+    for c, tau in ((1.0, 0.5), (6.0, 2.0)):
+        v, _ = s.value_grad(x, np.full(64, c, np.float32), tau)
+        exact = x.astype(np.float64) @ a + 0.3 - c * 0.01 * tau * (a @ a) / 2
+        np.testing.assert_allclose(v.cpu().numpy(), exact, rtol=0, atol=2e-5)
+
+
+def test_laplace_proposal_solve_slice(O):
+    s, P = pair(O, n=3, delta=0.01, T=1.0, K=2, Kp=3, N=2500, system="dubins_rel",
+                target="disk", tgt_params=(5.0,), proposal="laplace")
+    _compare_solve(O, s, P, _grid(-12, 12, 7, 3, (0, 0, math.pi / 2)), qid_base=3)
