@@ -50,13 +50,17 @@ class ContractionReport:
 
 
 def solve_adaptive(solver, x, tol: float, max_iter: int, qid_base: int = 0, qid=None,
-                   drift=None, allreduce=None, want_dv: bool = True):
+                   drift=None, allreduce=None, want_dv: bool = True, log=None):
     """Run Algorithm 1 per horizon until ε_j(k) < tol or max_iter passes.
 
     allreduce(partials[K][3] float64) -> partials: combine shards (sum cols 0–1, max col 2);
-    None for a single process. Returns a dict: v, dv, c [K][M](…) device tensors of each
-    horizon's final iterate, iters [K], eps [K][max_iter], d_sup [K][max_iter] (NaN past the
-    stop), tube [M] = min(g, min_j v_j), converged [K]."""
+    None for a single process. log: optional callable receiving one JSON-serialisable record
+    per Picard iteration (k, active horizons, ε_j(k), sup-norm differences, wall ms, max|v|,
+    min/max c over the active rows; the per-iteration record of S:316–317). Returns a dict:
+    v, dv, c [K][M](…) device tensors of each horizon's final iterate, iters [K],
+    eps [K][max_iter], d_sup [K][max_iter] (NaN past the stop), tube [M] = min(g, min_j v_j),
+    converged [K]."""
+    import time
     t = solver.torch
     cfg = solver.cfg
     x = solver._as_dev(x)
@@ -80,6 +84,8 @@ def solve_adaptive(solver, x, tol: float, max_iter: int, qid_base: int = 0, qid=
     for k in range(max_iter):
         if not active.any():
             break
+        t0 = time.perf_counter()
+        was_active = np.flatnonzero(active)
         solver._check(L.hjmc_picard_pass(
             solver.h, k, active.ctypes.data_as(C.c_void_p), C.c_void_p(v.data_ptr()),
             C.c_void_p(dv.data_ptr()) if dv is not None else None, C.c_void_p(c.data_ptr()),
@@ -91,6 +97,14 @@ def solve_adaptive(solver, x, tol: float, max_iter: int, qid_base: int = 0, qid=
             dsup[j, k] = tot[j, 2]
             if eps[j, k] < tol:
                 active[j] = 0
+        if log is not None:
+            rows = t.as_tensor(was_active, device=solver.device)
+            va, ca = v.index_select(0, rows), c.index_select(0, rows)
+            log({"k": k, "horizons": [int(j) + 1 for j in was_active],
+                 "eps": [float(eps[j, k]) for j in was_active],
+                 "d_sup": [float(dsup[j, k]) for j in was_active],
+                 "ms": 1e3 * (time.perf_counter() - t0), "max_abs_v": float(va.abs().max()),
+                 "c_min": float(ca.min()), "c_max": float(ca.max())})
     g, _ = solver.eval_target(x)
     tube = t.minimum(g, v.min(dim=0).values)
     return {"v": v, "dv": dv, "c": c, "iters": iters, "eps": eps, "d_sup": dsup, "tube": tube,
