@@ -85,3 +85,34 @@ def test_gloo_world2_gather_is_bit_identical(oracle_mod):
     part = O.residual_partials(ref["vhist"].astype(np.float32).astype(np.float64),
                                ref["g0"].astype(np.float32).astype(np.float64))
     np.testing.assert_allclose(eps, np.sqrt(part[..., 0] / part[..., 1]), rtol=1e-10)
+
+
+def _allreduce_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_18566_b200.picard import torch_allreduce
+
+        part = np.array([[1.0 + rank, 10.0 * (rank + 1), 0.5 * rank],
+                         [2.0, 3.0, 7.0 - rank]], dtype=np.float64)
+        out = torch_allreduce()(part)
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_picard_partials_allreduce():
+    """Algorithm 1's slice-wide stopping test across ranks: sums of (num, den), max of sup-norm."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_allreduce_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = q.get(timeout=120)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    np.testing.assert_array_equal(out, [[3.0, 30.0, 0.5], [4.0, 6.0, 7.0]])
