@@ -152,6 +152,13 @@ extern "C" {
  * are copied instead of recomputed (Algorithm 1's convergence test at ε = 0, per query).
  * Outputs are identical with and without the flag; hjmc_pass_count() reports the work done. */
 #define HJMC_FLAG_SKIP_STATIONARY 2u
+/* With crn = 1: a Φ pass is a pure function of its frozen coefficient c (same samples; the
+ * log-sum-exp shift and the proposal follow from c), so a pass whose c equals, bit for bit,
+ * the c of an earlier pass of the same (query, horizon) reuses that pass's sums instead of
+ * re-sampling (up to 8 distinct c per unit are kept). This shortcuts the Picard 2-cycles
+ * between the clamps c_min ↔ c_max that dominate the game slices (R8, R27). Outputs are
+ * identical with and without the flag; hjmc_pass_count() reports the sample passes run. */
+#define HJMC_FLAG_REUSE_PASSES 4u
 
 /* Sampling proposal of a Φ pass (reading R28).
  *  PLAIN:   y_i = x + bτ + σ z_i — the estimator of Cor. logsumexp / mc_gradient.
@@ -316,7 +323,8 @@ HJMC_API int hjmc_debug_normals(hjmc_handle* h, uint32_t qid, uint32_t jw, uint3
 HJMC_API int hjmc_check(hjmc_handle* h, void* stream);
 
 /* Number of Φ passes (each N samples of one query) the device executed since the previous call
- * (synchronises stream). Without HJMC_FLAG_SKIP_STATIONARY a solve_slice executes M·K·Kp. */
+ * (synchronises stream). Without HJMC_FLAG_SKIP_STATIONARY / HJMC_FLAG_REUSE_PASSES a
+ * solve_slice executes M·K·Kp. */
 HJMC_API int hjmc_pass_count(hjmc_handle* h, void* stream, uint64_t* passes);
 
 /* Smallest global query id that failed numerically since the last hjmc_check, or −1. */

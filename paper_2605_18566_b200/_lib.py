@@ -21,6 +21,7 @@ AVOIDS = {"none": 0, "disk": 1}
 VISC = {"paper": 0, "full": 1}
 FLAG_SYNC_CHECK = 1
 FLAG_SKIP_STATIONARY = 2
+FLAG_REUSE_PASSES = 4
 PROPOSALS = {"plain": 0, "laplace": 1}
 
 EXPORTS = [

@@ -107,6 +107,7 @@ void fill_common(const hjmc_handle* h, SolveParams* p) {
   p->err = h->d_err;
   p->bad = h->d_bad;
   p->skip_stationary = (h->cfg.flags & HJMC_FLAG_SKIP_STATIONARY) ? 1 : 0;
+  p->reuse_passes = (h->cfg.flags & HJMC_FLAG_REUSE_PASSES) ? 1 : 0;
   p->passes = h->d_passes;
 }
 
@@ -171,7 +172,7 @@ int hjmc_create(const hjmc_config* cfg, hjmc_handle** out) {
   if (c.antithetic != 0 && c.antithetic != 1) return fail(nullptr, HJMC_EINVAL, "antithetic must be 0 or 1");
   if (c.proposal != HJMC_PROPOSAL_PLAIN && c.proposal != HJMC_PROPOSAL_LAPLACE)
     return fail(nullptr, HJMC_EINVAL, "proposal must be PLAIN or LAPLACE");
-  if (c.flags & ~(HJMC_FLAG_SYNC_CHECK | HJMC_FLAG_SKIP_STATIONARY))
+  if (c.flags & ~(HJMC_FLAG_SYNC_CHECK | HJMC_FLAG_SKIP_STATIONARY | HJMC_FLAG_REUSE_PASSES))
     return fail(nullptr, HJMC_EINVAL, "unknown flag bits");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -553,6 +554,7 @@ int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, float* v,
   p.n_active = (int)act.size();
   p.kiter = k;
   p.skip_stationary = 0;
+  p.reuse_passes = 0;
   e = h->ks.solve(p, M * (int64_t)act.size(), s);
   if (e != cudaSuccess) return cuda_fail(h, e, "picard pass launch");
   e = launch_picard_residual(vout, h->d_vprev, M, h->d_active, (int)act.size(), h->d_partial,

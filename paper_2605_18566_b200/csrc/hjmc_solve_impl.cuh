@@ -145,10 +145,21 @@ __device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float 
   return amax;
 }
 
+// Pass memo (HJMC_FLAG_REUSE_PASSES): under CRN a Φ pass of one (query, horizon) is a pure
+// function of its frozen coefficient c (same samples, and A, B, the proposal centre and the
+// fallback shift all follow from c), so a pass at a c already seen by this unit returns the
+// stored CTA sums instead of re-sampling. The C2 trajectories cycle between the two clamps
+// (e.g. c_min, c_max, c_min, …; R8), which the stationary skip alone cannot shortcut.
+constexpr int kMemo = 8;
+
 template <int NDIM, int NT>
 struct SolveSmem {
   float part[NT / 32][NDIM + 1];
   double sum[NDIM + 1];
+  double memo_sum[kMemo][NDIM + 1];
+  double memo_c[kMemo];
+  float memo_B[kMemo];
+  int n_memo;
   double dg[NDIM];  // Dg(x + bτ) for the Laplace proposal (R28)
   float fmax_part[NT / 32];
   double c_next;
@@ -431,6 +442,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
   if (threadIdx.x == 0) {
     sm.c_next = unit_prologue<Tgt, NDIM>(P, tgt, m, j, sigma_d, xs, sm.dg);
     sm.shift = (sigma_d == 0.0) ? 1.f : 0.f;
+    sm.n_memo = 0;
   }
   __syncthreads();
   double c = sm.c_next;
@@ -439,6 +451,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
 
   const uint32_t jw = (P.mode != kModeValueGrad) ? (uint32_t)j : P.jtag;
   unsigned passes = 0;  // Φ passes this unit executed (thread 0)
+  const bool memo_on = P.reuse_passes && P.crn && P.mode == kModeSolve;
 
   for (int k = 0; k < P.Kp; ++k) {
     const uint32_t kw = (P.mode == kModeSolve)  ? (P.crn ? 0u : (uint32_t)k)
@@ -475,65 +488,87 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
     // every a_i = A core_i + B (+ tilt) ≤ 0: no weight can overflow
     float B = opaque(-A * tgt.core_lower(ctr, sigma) - tilt_max);
 
-    if constexpr (kLG) {
-      float S, Mb[12], amax;
-      lg_pass<NDIM, NT, false>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax);
-      lg_reduce<NDIM, NT>(sm, S, Mb);
-    } else {
-      float S, Mz[NDIM];
-      if (P.proposal)
-        mc_accumulate<Tgt, NDIM, NT, true>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base, id,
-                                           P.tag, P.rk, S, Mz, tz);
-      else
-        mc_accumulate<Tgt, NDIM, NT, false>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
-                                            id, P.tag, P.rk, S, Mz, tz);
-      cta_reduce<NDIM, NT>(sm, S, Mz);
-    }
-    if (!(sm.sum[0] >= (double)kUnderflowS)) {
-      // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with
-      // the exact maximum exponent, the plain two-pass log-sum-exp.
-      float amax_t;
+    int hit = -1;  // CTA-uniform: every thread reads the same memo after the last barrier
+    if (memo_on)
+      for (int e = 0; e < sm.n_memo; ++e)
+        if (sm.memo_c[e] == c) {
+          hit = e;
+          break;
+        }
+    if (hit < 0) {
       if constexpr (kLG) {
-        float S, Mb[12];
-        lg_pass<NDIM, NT, true>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax_t);
-      } else {
-        amax_t = mc_max_exponent<Tgt, NDIM, NT>(tgt, ctr, sigma_s, A, P.N, P.antithetic, w1base,
-                                                id, P.tag, P.rk, tz);
-      }
-      const float amax = warp_max(amax_t);
-      if ((threadIdx.x & 31) == 0) sm.fmax_part[threadIdx.x >> 5] = amax;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        float mx = sm.fmax_part[0];
-        for (int w = 1; w < NT / 32; ++w) mx = fmaxf(mx, sm.fmax_part[w]);
-        sm.shift = mx;
-      }
-      __syncthreads();
-      B = -sm.shift;
-      if constexpr (kLG) {
-        float S, Mb[12], am;
-        lg_pass<NDIM, NT, false>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, am);
+        float S, Mb[12], amax;
+        lg_pass<NDIM, NT, false>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax);
         lg_reduce<NDIM, NT>(sm, S, Mb);
       } else {
         float S, Mz[NDIM];
         if (P.proposal)
-          mc_accumulate<Tgt, NDIM, NT, true>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
-                                             id, P.tag, P.rk, S, Mz, tz);
+          mc_accumulate<Tgt, NDIM, NT, true>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base, id,
+                                             P.tag, P.rk, S, Mz, tz);
         else
           mc_accumulate<Tgt, NDIM, NT, false>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
                                               id, P.tag, P.rk, S, Mz, tz);
         cta_reduce<NDIM, NT>(sm, S, Mz);
       }
-    }
+      if (!(sm.sum[0] >= (double)kUnderflowS)) {
+        // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with
+        // the exact maximum exponent, the plain two-pass log-sum-exp.
+        float amax_t;
+        if constexpr (kLG) {
+          float S, Mb[12];
+          lg_pass<NDIM, NT, true>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax_t);
+        } else {
+          amax_t = mc_max_exponent<Tgt, NDIM, NT>(tgt, ctr, sigma_s, A, P.N, P.antithetic, w1base,
+                                                  id, P.tag, P.rk, tz);
+        }
+        const float amax = warp_max(amax_t);
+        if ((threadIdx.x & 31) == 0) sm.fmax_part[threadIdx.x >> 5] = amax;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          float mx = sm.fmax_part[0];
+          for (int w = 1; w < NT / 32; ++w) mx = fmaxf(mx, sm.fmax_part[w]);
+          sm.shift = mx;
+        }
+        __syncthreads();
+        B = -sm.shift;
+        if constexpr (kLG) {
+          float S, Mb[12], am;
+          lg_pass<NDIM, NT, false>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, am);
+          lg_reduce<NDIM, NT>(sm, S, Mb);
+        } else {
+          float S, Mz[NDIM];
+          if (P.proposal)
+            mc_accumulate<Tgt, NDIM, NT, true>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
+                                               id, P.tag, P.rk, S, Mz, tz);
+          else
+            mc_accumulate<Tgt, NDIM, NT, false>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
+                                                id, P.tag, P.rk, S, Mz, tz);
+          cta_reduce<NDIM, NT>(sm, S, Mz);
+        }
+      }
+    }  // hit < 0
     if (threadIdx.x == 0) {
+      const double* sums = sm.sum;
+      if (hit >= 0) {
+        sums = sm.memo_sum[hit];
+        B = sm.memo_B[hit];
+      } else {
+        ++passes;
+        if (memo_on && sm.n_memo < kMemo) {
+          const int e = sm.n_memo;
+          sm.memo_c[e] = c;
+          sm.memo_B[e] = B;
+          for (int d = 0; d <= NDIM; ++d) sm.memo_sum[e][d] = sm.sum[d];
+          sm.n_memo = e + 1;
+        }
+      }
       bool done = false;
       double dsh[NDIM];
       if (P.proposal)
         for (int d = 0; d < NDIM; ++d) dsh[d] = ((double)ctr[d] - (double)xs[d]) / sigma_d;
-      sm.c_next = pass_epilogue<Tgt, NDIM>(P, tgt, m, j, k, id, c, sigma_d, A, B, core_ref, sm.sum,
+      sm.c_next = pass_epilogue<Tgt, NDIM>(P, tgt, m, j, k, id, c, sigma_d, A, B, core_ref, sums,
                                            P.proposal ? dsh : nullptr, &done);
       sm.shift = done ? 1.f : 0.f;
-      ++passes;
     }
     __syncthreads();
     c = sm.c_next;

@@ -33,6 +33,7 @@ class SolverConfig:
     device: int = 0
     sync_check: bool = False
     skip_stationary: bool = False
+    reuse_passes: bool = False   # HJMC_FLAG_REUSE_PASSES (exact pass memo under CRN)
     system: str = "quadratic"
     sys_params: tuple = ()
     target: str = "quad_bowl"
@@ -60,7 +61,8 @@ class SolverConfig:
         c.m0, c.c_min, c.c_max, c.tag, c.device = self.m0, self.c_min, self.c_max, self.tag, self.device
         c.proposal = _lib.PROPOSALS[self.proposal]
         c.flags = (_lib.FLAG_SYNC_CHECK if self.sync_check else 0) | (
-            _lib.FLAG_SKIP_STATIONARY if self.skip_stationary else 0)
+            _lib.FLAG_SKIP_STATIONARY if self.skip_stationary else 0) | (
+            _lib.FLAG_REUSE_PASSES if self.reuse_passes else 0)
         return c
 
 

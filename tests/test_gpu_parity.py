@@ -300,6 +300,48 @@ def test_skip_stationary_is_bit_identical():
     assert nocrn.pass_count() == M * 3 * 5
 
 
+@pytest.mark.parametrize("skip", [False, True])
+def test_reuse_passes_is_bit_identical(skip):
+    """HJMC_FLAG_REUSE_PASSES: under CRN a pass is a function of its c, so a pass at a c the
+    unit has already used returns the stored sums. Every output equals the full schedule bit
+    for bit, and the number of sample passes equals the number of distinct c per (query,
+    horizon) trajectory (read off the full run's own chist), stationary skip or not."""
+    kw = dict(N=3000, K=3, Kp=8)
+    base = Solver(SolverConfig.from_preset(I.C2, **kw))
+    memo = Solver(SolverConfig.from_preset(I.C2, reuse_passes=True, skip_stationary=skip, **kw))
+    x = I.queries(I.C2)[::7]
+    a = base.solve_slice(x)
+    base.pass_count()
+    b = memo.solve_slice(x)
+    nb = memo.pass_count()
+    for k in a:
+        assert torch.equal(a[k], b[k]), k
+    ch = a["chist"].cpu().numpy()                     # [K][Kp][M]
+    distinct = sum(len(set(ch[j, :, m].tolist())) for j in range(ch.shape[0])
+                   for m in range(ch.shape[2]))
+    assert nb == distinct
+    assert nb < 0.5 * x.shape[0] * 3 * 8               # the C2 slice cycles between the clamps
+    # without CRN every pass draws fresh samples: nothing is reused
+    nocrn = Solver(SolverConfig.from_preset(I.C2, reuse_passes=True, crn=False, **kw))
+    nocrn.solve_slice(x)
+    assert nocrn.pass_count() == x.shape[0] * 3 * 8
+
+
+def test_reuse_passes_lane_groups_and_proposal():
+    """The memo is shared by the lane-group kernel (n = 45 pair union) and the Laplace
+    proposal (the centre μ follows from c): outputs bit-identical to the full schedule."""
+    for preset, extra in ((I.C5.with_(N=2048, K=2, Kp=4, grid_pts=8), {}),
+                          (I.C2.with_(N=2048, K=2, Kp=6, grid_pts=11), {"proposal": "laplace"})):
+        x = I.queries(preset)
+        base = Solver(SolverConfig.from_preset(preset, **extra))
+        memo = Solver(SolverConfig.from_preset(preset, reuse_passes=True, **extra))
+        a = base.solve_slice(x)
+        b = memo.solve_slice(x)
+        for k in a:
+            assert torch.equal(a[k], b[k]), (preset.name, k)
+        assert memo.pass_count() <= x.shape[0] * preset.K * preset.Kp
+
+
 def test_picard_stepwise_equals_fused_solve():
     """hjmc_picard_pass with every horizon active reproduces hjmc_solve_slice's iterates
     bit for bit (same counters, same kernel body)."""
