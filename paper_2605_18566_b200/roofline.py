@@ -3,9 +3,17 @@
 The path is bound by plain ALU/MUFU arithmetic (no contraction, ~0 HBM traffic),
 so its roofline is a pipe roofline. Per eval the METHOD needs (independent of how the kernel
 is written; DESIGN.md §6 derives each line):
-  * Philox4x32-10, one call per 4 normals (draw layout R19 wastes none for n = 2, 3, 6):
-    10 rounds × (2 wide multiplies + 2 three-input XORs); in the first two rounds counter
-    words 1–3 are the same for every sample, leaving 18 multiplies and 19 XORs per call;
+  * Philox4x32-10, one call (block) per 4 normals (draw layout R19 wastes none for n = 2, 3,
+    6): 10 rounds × (2 wide multiplies + 2 three-input XORs). Under the counter contract
+    (c0 = draw group g, c1 = block | kw<<8 | jw<<16, c2 = query id, c3 = tag) the values that
+    depend on neither g nor the block are per-unit constants, and those that depend on g but
+    not on the block are shared by the Q blocks of a group. Tracing the rounds:
+      multiplies: R1 (g·M0 shared, qid·M1 constant), R2 (b-only: constant; g-only: shared),
+                  R3 (one shared, one per block), R4–R10 (2 per block) → 3 per group + 15 per block;
+      XORs:       R1 (one b-only constant, one shared), R2 (one shared, one per block),
+                  R3–R10 (2 per block)                                → 2 per group + 17 per block;
+    the minimum any kernel honouring the contract must execute (the C2 kernel's SASS has
+    exactly 48 IMAD.WIDE and 53 XOR-LOP3 per 3-block group);
   * Box–Muller per pair: 2 mantissa builds, 1 add, LG2 + SQRT + COS + SIN, 2 multiplies;
   * y = x + σ z on the coordinates g reads, g itself, a = A·core + B (1 FFMA), 1 EX2;
   * the moment update: 1 add + n FFMAs.
@@ -37,15 +45,16 @@ def op_counts(n: int, target: str, antithetic: bool = False) -> dict:
     """Minimal lane-operation counts per eval, by pipe class (antithetic: one draw of n
     normals serves two samples, so the draw costs are halved).
 
-    Per draw (grouped layout): Q/G Philox calls of 18 sample-dependent wide multiplies and 19
-    XORs; per Box–Muller pair 2 mantissa builds (ALU), u = F − (1 − 2⁻²⁴) and r̂·cos, r̂·sin
-    (3 FP32), LG2 + SQRT + COS + SIN (4 MUFU; the angle a is already in revolutions, the MUFU
-    unit's native unit); a pair whose second normal is unused drops its SIN and one multiply."""
+    Per draw group (grouped layout): Q Philox blocks, 3 + 15Q wide multiplies and 2 + 17Q
+    XORs (module docstring); per Box–Muller pair 2 mantissa builds (ALU), u = F − (1 − 2⁻²⁴)
+    and r̂·cos, r̂·sin (3 FP32), LG2 + SQRT + COS + SIN (4 MUFU; the angle a is already in
+    revolutions, the MUFU unit's native unit); a pair whose second normal is unused drops its
+    SIN and one multiply. Divided by the G draws of the group."""
     G, Q = draw_layout(n)
     used = G * n                                # normals used per group
     pairs = (used + 1) // 2
     half = used % 2                             # a last pair with only its cos used
-    draw = {"imul": 18 * Q / G, "alu": (19 * Q + 2 * pairs) / G + 1,
+    draw = {"imul": (3 + 15 * Q) / G, "alu": (2 + 17 * Q + 2 * pairs) / G,
             "fp32": (3 * pairs - half) / G, "mufu": (4 * pairs - half) / G}
     # ---- per sample: y, g, weight, moments
     samp = {"imul": 0, "alu": 0, "fp32": 0, "mufu": 1}   # EX2
