@@ -1,0 +1,91 @@
+"""The roofline's algorithmic Philox counts (paper_2605_18566_b200/roofline.py) against the
+compiled sm_100a SASS of the solve kernels' hot loops (cuobjdump, no GPU needed).
+
+roofline.op_counts claims the minimum number of 32×32→64 multiplies and XORs a kernel honouring
+the counter contract (R19) must execute per eval: 3 + 15·Q multiplies and 2 + 17·Q XORs per
+draw group of Q blocks. If the kernel executed fewer, the roofline would over-state the
+Philox work (and the achieved fraction); more means waste the fraction must absorb. The
+generic kernels must match exactly; the n = 45 lane-group kernel re-derives the per-group
+constants in each of its 4 lanes (documented in DESIGN.md §6)."""
+import os
+import re
+import shutil
+import subprocess
+import sys
+from collections import Counter
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+pytestmark = pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump missing")
+
+
+@pytest.fixture(scope="module")
+def funcs():
+    from paper_2605_18566_b200 import build
+
+    lib = build.build()
+    from sass_loop import functions
+
+    return functions(lib)
+
+
+def hot_loop_counts(funcs, pattern, n=None):
+    """Instruction histogram of the kernel's tightest plain sample loop (fewest instructions per
+    EX2 among loops with one EX2 per drawn sample, i.e. not the antithetic ±z loops) and its EX2
+    count (= samples per loop trip)."""
+    from sass_loop import loops
+
+    from paper_2605_18566_b200 import roofline as RL
+
+    name = next(k for k in funcs if pattern in k)
+    cands = []
+    for ex2, body in loops(funcs[name]):
+        ops = Counter((t.split()[1] if t.startswith("@") else t.split()[0]) for _, t in body)
+        if n is not None:
+            G, Q = RL.draw_layout(n)
+            groups = ops["MUFU.LG2"] / ((G * n + 1) // 2)
+            if ex2 != round(groups * G):
+                continue
+        cands.append((len(body) / ex2, ex2, body, ops))
+    _, ex2, body, ops = min(cands, key=lambda c: c[0])
+    xors = sum(1 for _, t in body if "LOP3.LUT" in t and re.search(r"0x(96|3c)\b", t))
+    return ops, xors, ex2
+
+
+@pytest.mark.parametrize("pattern,n,target", [
+    ("DiskILi3EEELi3ELi256ELb0", 3, "disk"),
+    ("RelDisk6ILi6EEELi6ELi256ELb0", 6, "rel_disk6"),
+    ("PairUnionILi15EEELi15ELi256ELb0", 15, "pair_union"),
+])
+def test_generic_kernels_execute_the_minimal_philox_work(funcs, pattern, n, target):
+    from paper_2605_18566_b200 import roofline as RL
+
+    ops, xors, ex2 = hot_loop_counts(funcs, pattern, n)
+    want = RL.op_counts(n, target)
+    # multiplies: the minimum, up to 1 % (n = 15: ptxas rematerialises one hoisted per-block
+    # product inside the 2-sample unrolled loop, 127 for 2 × 63)
+    imul = ops["IMAD.WIDE.U32"] / ex2
+    assert want["imul"] <= imul <= 1.01 * want["imul"]
+    G, Q = RL.draw_layout(n)
+    # XORs: the minimum, plus at most one per group (ptxas splits round 2's
+    # hi(b-product) ^ lo(g·M0) ^ key into a shared 2-input XOR and a per-block one)
+    per_group = xors / ex2 * G
+    assert 2 + 17 * Q <= per_group <= 3 + 17 * Q
+    # MUFU: the Box–Muller + target + EX2 count of the roofline, nothing more
+    mufu = sum(c for op, c in ops.items() if op.startswith("MUFU."))
+    assert mufu / ex2 == pytest.approx(want["mufu"])
+
+
+def test_lane_group_kernel_overhead_is_the_documented_one(funcs):
+    """n = 45 lane groups: each lane draws 3 blocks with its own 3 per-group multiplies
+    (4 × (3 + 45) = 192 per sample vs the minimum 3 + 15·12 = 183) and evaluates the weight
+    (SQRT + EX2) redundantly in all 4 lanes."""
+    from paper_2605_18566_b200 import roofline as RL
+
+    ops, xors, ex2 = hot_loop_counts(funcs, "PairUnionILi45EEELi45ELi256ELb1")
+    assert ex2 == 1
+    assert RL.op_counts(45, "pair_union")["imul"] == 183
+    assert 4 * ops["IMAD.WIDE.U32"] == 192
