@@ -102,16 +102,75 @@ __global__ void __launch_bounds__(256, 4) mix(float* out, Stamp* st, uint32_t k0
   if (threadIdx.x == 0) st[blockIdx.x] = Stamp{t0, t1, smid()};
 }
 
+// Parametric variant for pricing alternatives: the Philox integer share as above, kM MUFU
+// (cycling LG2, SQRT, COS, EX2) and kF dependent FFMAs per eval — e.g. (8, 14) ≈ today's C2
+// mix, (7, 24) ≈ one MUFU traded for a 10-FFMA polynomial, (6, 34), (5, 44).
+template <int kM, int kF>
+__global__ void __launch_bounds__(256, 4) pmix(float* out, Stamp* st, uint32_t k0, float p1) {
+  uint32_t u[kChains], w[kChains];
+  float f[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) {
+    u[c] = threadIdx.x * 2654435761u + c;
+    w[c] = u[c] ^ 0x5bd1e995u;
+    f[c] = 0.25f + threadIdx.x * 1e-4f + c * 1e-2f;
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+#pragma unroll
+      for (int r = 0; r < 6; ++r) {
+        uint32_t h0, l0, h1, l1;
+        mulw(u[c], 0xD2511F53u, h0, l0);
+        mulw(w[c], 0xCD9E8D57u, h1, l1);
+        u[c] = h1 ^ l0 ^ (k0 + r);
+        w[c] = h0 ^ l1 ^ (k0 * 3u + r);
+      }
+      u[c] ^= w[c] ^ k0;
+      w[c] ^= u[c] ^ 0x9E3779B9u;
+      u[c] ^= w[c] ^ 0x7F4A7C15u;
+      w[c] ^= u[c] ^ k0;
+      float x = __uint_as_float((u[c] >> 9) | 0x3F800000u) * f[c];
+      float y = x;
+#pragma unroll
+      for (int m = 0; m < kM; ++m) {
+        const float a = (m & 1) ? y : x;
+        float r;
+        switch (m & 3) {
+          case 0: r = lg2a(a); break;
+          case 1: r = sqrta(fabsf(a)); break;
+          case 2: r = cosa(a); break;
+          default: r = ex2a(-fabsf(a)); break;
+        }
+        if (m & 1) y = r; else x = r;
+      }
+      float t = x + y;
+#pragma unroll
+      for (int q = 0; q < kF; ++q) t = fmaf(t, p1, (q & 1) ? x : y);
+      f[c] = t * 0.5f + 0.25f;
+    }
+  }
+  __syncthreads();
+  const long long t1 = clock64();
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) s += f[c] + (float)(u[c] & 1u);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) st[blockIdx.x] = Stamp{t0, t1, smid()};
+}
+
 // evals per SM clock: median over SMs of (evals of all CTAs on the SM) / (their clock window)
-template <bool A, bool B, bool C>
-double run(int nsm) {
+using Kern = void (*)(float*, Stamp*, uint32_t, float);
+double run(Kern k, int nsm) {
   const int ctas = nsm * 4, threads = 256;
   float* out;
   Stamp* st;
   cudaMalloc(&out, sizeof(float) * ctas * threads);
   cudaMalloc(&st, sizeof(Stamp) * ctas);
-  mix<A, B, C><<<ctas, threads>>>(out, st, 0x9E3779B9u, 0.999f);
-  mix<A, B, C><<<ctas, threads>>>(out, st, 0x9E3779B9u, 0.999f);
+  k<<<ctas, threads>>>(out, st, 0x9E3779B9u, 0.999f);
+  k<<<ctas, threads>>>(out, st, 0x9E3779B9u, 0.999f);
   cudaDeviceSynchronize();
   std::vector<Stamp> h(ctas);
   cudaMemcpy(h.data(), st, sizeof(Stamp) * ctas, cudaMemcpyDeviceToHost);
@@ -134,11 +193,16 @@ int main() {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   struct R { const char* name; double evals_per_clk; int mufu; };
   std::vector<R> r;
-  r.push_back({"mufu_only", run<false, false, true>(nsm), 8});
-  r.push_back({"mufu+fp32", run<false, true, true>(nsm), 8});
-  r.push_back({"int_only", run<true, false, false>(nsm), 0});
-  r.push_back({"mufu+int", run<true, false, true>(nsm), 8});
-  r.push_back({"full_c2_mix", run<true, true, true>(nsm), 8});
+  r.push_back({"mufu_only", run(mix<false, false, true>, nsm), 8});
+  r.push_back({"mufu+fp32", run(mix<false, true, true>, nsm), 8});
+  r.push_back({"int_only", run(mix<true, false, false>, nsm), 0});
+  r.push_back({"mufu+int", run(mix<true, false, true>, nsm), 8});
+  r.push_back({"full_c2_mix", run(mix<true, true, true>, nsm), 8});
+  r.push_back({"p_int+8mufu+14ffma", run(pmix<8, 14>, nsm), 8});
+  r.push_back({"p_int+7mufu+24ffma", run(pmix<7, 24>, nsm), 7});
+  r.push_back({"p_int+6mufu+34ffma", run(pmix<6, 34>, nsm), 6});
+  r.push_back({"p_int+5mufu+44ffma", run(pmix<5, 44>, nsm), 5});
+  r.push_back({"p_int+8mufu+30ffma", run(pmix<8, 30>, nsm), 8});
   if (cudaGetLastError() != cudaSuccess) return 1;
   printf("{\n  \"what\": \"synthetic C2 instruction mix per eval: 8 MUFU, 12 IMAD.WIDE + 16 LOP3, ~14 FP32; "
          "evals per SM clock (median over SMs) and MUFU lane-ops/clk/SM (peak 16)\",\n  \"mixes\": {\n");
