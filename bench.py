@@ -114,8 +114,9 @@ class ClockSampler:
 
 
 # ---- CPU oracle (cpu_baseline leg and the reference arm) --------------------------------------
-def oracle_sample_run(preset, count: int, seed_offset: int = 0):
-    """Time the oracle, as it stands, on `count` queries of the workload (full K×Kp×N each)."""
+def oracle_sample_run(preset, count: int, seed_offset: int = 0, nthreads: int = 0):
+    """Time the oracle, as it stands, on `count` queries of the workload (full K×Kp×N each);
+    nthreads = 0 uses every host core (OpenMP over queries), 1 is the paper's setting."""
     import oracle as O
     from paper_2605_18566_b200 import inputs as I
 
@@ -125,10 +126,10 @@ def oracle_sample_run(preset, count: int, seed_offset: int = 0):
     ids = I.subsample_ids(x_all.shape[0], count)
     ids = (ids + seed_offset) % x_all.shape[0]
     t0 = time.perf_counter()
-    r = O.solve_slice(P, x_all[ids], qids=ids.astype(np.uint32))
+    r = O.solve_slice(P, x_all[ids], qids=ids.astype(np.uint32), nthreads=nthreads)
     dt = time.perf_counter() - t0
     evals = len(ids) * preset.N * preset.K * preset.Kp
-    return evals / dt, dt, len(ids), O.max_threads(), r
+    return evals / dt, dt, len(ids), (nthreads or O.max_threads()), r
 
 
 def auto_sample(preset) -> int:
@@ -314,6 +315,11 @@ def run_ours(args):
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{used} of {M} queries (deterministic spread), full K×Kp×N per query; "
                          f"{dt:.1f} s wall on {cores} threads"}
+        # the paper's setting: one CPU core, on a proportionally smaller sample
+        n1 = max(1, count // max(cores, 1))
+        v1, dt1, used1, _, _ = oracle_sample_run(preset, n1, seed_offset=7, nthreads=1)
+        cpu["single_core"] = {"value": v1, "unit": UNIT, "cores": 1,
+                              "sample": f"{used1} queries, {dt1:.1f} s wall on 1 thread"}
 
     slices = world
     line = {

@@ -426,8 +426,8 @@ int orc_solve_slice(const orc_problem* P, const float* x, const float* drift, co
   int status = 0;
   int64_t units = M * (int64_t)K;
 #ifdef _OPENMP
-  if (nthreads > 0) omp_set_num_threads(nthreads);
-#pragma omp parallel for schedule(dynamic, 1)
+  const int nt = nthreads > 0 ? nthreads : omp_get_max_threads();  /* per call, not global */
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
 #endif
   for (int64_t u = 0; u < units; ++u) {
     int64_t m = u / K;
@@ -498,7 +498,7 @@ int orc_picard_adaptive(const orc_problem* P, const float* x, const uint32_t* qi
   if (!vprev || !vcur || !c) { free(vprev); free(vcur); free(c); return 1; }
   int status = 0;
 #ifdef _OPENMP
-  if (nthreads > 0) omp_set_num_threads(nthreads);
+  const int nt = nthreads > 0 ? nthreads : omp_get_max_threads();  /* per call, not global */
 #endif
   for (int j = 1; j <= K; ++j) {
     double tau = (double)j * P->T / (double)K;
@@ -517,7 +517,7 @@ int orc_picard_adaptive(const orc_problem* P, const float* x, const uint32_t* qi
     for (k = 0; k < max_iter; ++k) {
       uint32_t kw = P->crn ? 0u : (uint32_t)k;
 #ifdef _OPENMP
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
 #endif
       for (int64_t m = 0; m < M; ++m) {
         double xm[ORC_MAX_N], dvm[ORC_MAX_N];
