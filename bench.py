@@ -236,6 +236,28 @@ def run_ours(args):
     value = evals_step_rank * world * args.steps / (total_ms / 1000.0)
     kern_avg_ms = kern_sum / args.steps
 
+    # ---- the per-slice result gather (north_star: the only NCCL traffic), timed separately:
+    # every rank's (v, dv, c, tube) all-gathered over NVLink after the solve --------------------
+    gather = None
+    if world > 1:
+        from paper_2605_18566_b200 import shard
+
+        res = {k: out[k] for k in ("v", "dv", "c", "tube")}
+        shard.gather_results(res, M * world)              # warm the communicator
+        torch.cuda.synchronize(dev)
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        full = shard.gather_results(res, M * world)
+        g1.record(stream)
+        torch.cuda.synchronize(dev)
+        gt = torch.tensor([g0.elapsed_time(g1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+        gather = {"ms": float(gt[0]), "collective": "NCCL all_gather (torch.distributed)",
+                  "bytes_per_rank": int(sum(t.numel() * 4 for t in res.values())),
+                  "bytes_gathered": int(sum(t.numel() * 4 for t in full.values())),
+                  "share_of_step": float(gt[0]) / (total_ms / args.steps)}
+
     # ---- end to end: host buffers through hjmc_solve_slice_host (copies inside) ----------
     e2e = None
     if True:
@@ -337,6 +359,7 @@ def run_ours(args):
         "roofline": roof,
         "e2e": e2e,
         "fastpath": fastpath,
+        "gather": gather,
         "cpu_baseline": cpu,
         "clocks": clk,
         "paper_context": "paper: 14–26 s per 40×40 slice (N=14,000) on one CPU core (P:474)",
