@@ -19,10 +19,13 @@ from paper_2605_18566_b200.solver import Solver, SolverConfig  # noqa: E402
 SUBSET = {1: None, 2: None, 3: 4096, 4: 2048, 5: 1184}
 
 
-def run(idx):
+def run(idx, full_slice=False):
     p = I.BY_INDEX[idx]
     x_all = I.queries(p)
     sub = SUBSET[idx]
+    if full_slice:      # one complete 2-D slice (the first), measured rather than extrapolated
+        sub = None
+        x_all = x_all[: p.grid_pts * p.grid_pts]
     ids = np.arange(x_all.shape[0]) if sub is None else I.subsample_ids(x_all.shape[0], sub)
     s = Solver(SolverConfig.from_preset(p))
     x = torch.from_numpy(x_all[ids]).cuda()
@@ -55,6 +58,7 @@ def run(idx):
     r = {"config": p.name, "queries": int(len(ids)), "ms": ms, "evals_per_s": evals / (ms / 1e3),
          "frac_of_roofline": evals / (ms / 1e3) / rl["peak_evals_per_s"], "binding": rl["binding_pipe"],
          "full_slice_s_extrapolated": p.M * p.N * p.K * p.Kp / (evals / (ms / 1e3)) / len(p.slices),
+         "measured_full_slice": bool(full_slice),
          "fastpath": {"ms": fms, "passes_frac": fpasses / (len(ids) * p.K * p.Kp),
                       "full_slice_s_extrapolated": ms and fms / ms * p.M * p.N * p.K * p.Kp
                       / (evals / (ms / 1e3)) / len(p.slices)}}
@@ -64,4 +68,4 @@ def run(idx):
 if __name__ == "__main__":
     which = [int(a.lstrip("c")) for a in sys.argv[1:] if a.startswith("c")] or [2, 3, 4, 5]
     for i in which:
-        run(i)
+        run(i, full_slice="--full-slice" in sys.argv)
