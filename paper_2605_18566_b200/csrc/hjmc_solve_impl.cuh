@@ -23,10 +23,14 @@ namespace hjmc {
 #ifndef HJMC_UNROLL
 #define HJMC_UNROLL 2
 #endif
+#ifndef HJMC_LG_UNROLL
+#define HJMC_LG_UNROLL 2
+#endif
 
 namespace {
 
 constexpr int kSampleUnroll = HJMC_UNROLL;
+constexpr int kLgUnroll = HJMC_LG_UNROLL;
 constexpr double kLog2e = 1.4426950408889634074;
 constexpr double kLn2 = 0.69314718055994530942;
 constexpr float kUnderflowS = 7.888609052210118e-31f;  // 2^-100: fallback threshold
@@ -224,9 +228,9 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
 #pragma unroll
   for (int c = 0; c < 12; ++c) Mb[c] = 0.f;
   const uint32_t N = P.N;
-  const uint32_t iters = (N + kStride - 1) / kStride;
-  for (uint32_t t = 0; t < iters; ++t) {
-    const uint32_t i = t * kStride + slot;
+  // One sample per lane group per trip; trips where every slot's sample exists run without
+  // the i < N guard (C5: N = 2^20, all of them), the ragged last trip with it.
+  auto trip = [&](uint32_t i, bool guard) {
     float z[12];
 #pragma unroll
     for (int qd = 0; qd < 3; ++qd) {
@@ -245,7 +249,7 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
     best = fminf(best, __shfl_xor_sync(0xffffffffu, best, 1));
     best = fminf(best, __shfl_xor_sync(0xffffffffu, best, 2));
     const float core = sqrt_approx(best);
-    if (i < N) {
+    if (!guard || i < N) {
       if (kMaxMode) {
         amax = fmaxf(amax, A * core);
       } else {
@@ -255,7 +259,11 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
         for (int c = 0; c < 12; ++c) Mb[c] = fmaf(wt, z[c], Mb[c]);
       }
     }
-  }
+  };
+  const uint32_t full = N / kStride;
+#pragma unroll(kLgUnroll)
+  for (uint32_t t = 0; t < full; ++t) trip(t * kStride + slot, false);
+  if (full * kStride < N) trip(full * kStride + slot, true);
 }
 
 // Merge the lane-group sums into sm.sum (double), deterministic order.

@@ -7,12 +7,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2605_18566_b200 import build as B  # noqa: E402
 
+# (the warp-specialised HJMC_WS variants of an earlier revision were measured and removed)
 VARIANTS = {
-    "a_ws0": ["-DHJMC_WS=0"],
-    "b_ws_s4_p1": ["-DHJMC_WS=1", "-DHJMC_WS_STAGES=4", "-DHJMC_WS_SPT=1"],
-    "c_ws_s8_p1": ["-DHJMC_WS=1", "-DHJMC_WS_STAGES=8", "-DHJMC_WS_SPT=1"],
-    "d_ws_s2_p4": ["-DHJMC_WS=1", "-DHJMC_WS_STAGES=2", "-DHJMC_WS_SPT=4"],
-    "e_ws_s6_p2": ["-DHJMC_WS=1", "-DHJMC_WS_STAGES=6", "-DHJMC_WS_SPT=2"],
+    "lgu1": ["-DHJMC_LG_UNROLL=1"],
+    "lgu2": ["-DHJMC_LG_UNROLL=2"],
 }
 
 if __name__ == "__main__":
