@@ -404,14 +404,15 @@ __device__ __noinline__ double unit_prologue(const SolveParams& P, const Tgt& tg
 #define HJMC_NT 256
 #endif
 // Resident CTAs per SM requested from ptxas (caps registers: 4 → 64 regs at 256 threads).
-// Measured on B200 for C2 (n = 3): 4/SM beats 3/SM by 2% and 1/SM by 7% (profiles/). Larger n
-// needs the registers for z[n] and the moments, so the request relaxes with n.
+// Measured on B200: C2 (n = 3) 4/SM beats 3/SM by 2% and 1/SM by 7%; C4 (n = 15) 4/SM beats
+// 2/SM (128 regs, no spill) by 3.3% even with 1.5 spill loads per sample in the loop, and
+// 3/SM by 2%. Above n = 16 the generic path needs z[n] and the moments in registers (1/SM).
 #ifndef HJMC_MINB
 #define HJMC_MINB 0
 #endif
 template <int NDIM, bool kLG>
 constexpr int min_blocks() {
-  return HJMC_MINB > 0 ? HJMC_MINB : ((kLG || NDIM <= 6) ? 4 : (NDIM <= 16 ? 2 : 1));
+  return HJMC_MINB > 0 ? HJMC_MINB : ((kLG || NDIM <= 16) ? 4 : 1);
 }
 
 // kLG: the lane-group instantiation (non-antithetic passes of UseLaneGroups targets); it does

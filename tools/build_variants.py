@@ -11,6 +11,8 @@ from paper_2605_18566_b200 import build as B  # noqa: E402
 VARIANTS = {
     "lgu1": ["-DHJMC_LG_UNROLL=1"],
     "lgu2": ["-DHJMC_LG_UNROLL=2"],
+    "mb3": ["-DHJMC_MINB=3"],
+    "mb4": ["-DHJMC_MINB=4"],
 }
 
 if __name__ == "__main__":
