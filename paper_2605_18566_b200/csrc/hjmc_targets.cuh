@@ -92,8 +92,10 @@ struct RelDisk6 {  // g = ‖(y0 − y3, y1 − y4)‖ − r  (n = 6)
   __device__ explicit RelDisk6(const TargetParams& t) : off(-(t.np > 0 ? t.p[0] : 1.5f)) {}
   __device__ __forceinline__ float core(const float (&xs)[NDIM], float sigma,
                                         const float (&z)[NDIM]) const {
-    const float dx = fmaf(sigma, z[0], xs[0]) - fmaf(sigma, z[3], xs[3]);
-    const float dz = fmaf(sigma, z[1], xs[1]) - fmaf(sigma, z[4], xs[4]);
+    // (x0 − x3) + σ(z0 − z3): the x difference is loop-invariant (hoisted by the compiler),
+    // leaving one FADD + one FFMA per relative coordinate
+    const float dx = fmaf(sigma, z[0] - z[3], xs[0] - xs[3]);
+    const float dz = fmaf(sigma, z[1] - z[4], xs[1] - xs[4]);
     return sqrt_approx(fmaf(dx, dx, dz * dz));
   }
   __device__ float core_lower(const float (&xs)[NDIM], float sigma) const {

@@ -76,7 +76,7 @@ def op_counts(n: int, target: str, antithetic: bool = False) -> dict:
         samp["fp32"] += 4
         samp["mufu"] += 1
     elif target == "rel_disk6":
-        samp["fp32"] += 8
+        samp["fp32"] += 6                   # 2 × (z diff + FFMA), FMUL + FFMA for the norm²
         samp["mufu"] += 1
     samp["fp32"] += 1 + 1 + n               # a = A·core + B; S += w; M += w z
     f = 0.5 if antithetic else 1.0
