@@ -325,6 +325,21 @@ def run_ours(args):
             "kernel_ms_avg": kern_avg_ms}
     if clk and clk.get("sm_mhz"):
         roof["frac_at_measured_clock"] = roof["frac"] * 1965.0 / clk["sm_mhz"]
+    # the query / coefficient / result streams (north_star: "achieved HBM GB/s"): per unit the
+    # kernel reads x (n floats) and writes, per Picard iterate, vhist + chist, and per query
+    # v, dv, c, tube, g0 — algorithmic bytes over the kernel time, against the measured copy peak
+    hbm_bytes = 4 * (M * preset.K * preset.n + 2 * M * preset.K * preset.Kp
+                     + M * (preset.n + 4))
+    peaks_file = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm_peak = None
+    if os.path.exists(peaks_file):
+        with open(peaks_file) as fh:
+            hbm_peak = json.load(fh).get("hbm_gbs")
+    hbm_gbps = hbm_bytes / (kern_avg_ms / 1000.0) / 1e9
+    roof["hbm"] = {"algorithmic_bytes_per_launch": int(hbm_bytes), "achieved_gbps": hbm_gbps,
+                   "peak_gbps": hbm_peak,
+                   "frac": (hbm_gbps / hbm_peak) if hbm_peak else None,
+                   "note": "no sample touches HBM; the streams are queries and per-iterate results"}
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
