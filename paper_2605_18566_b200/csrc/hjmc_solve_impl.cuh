@@ -164,6 +164,8 @@ struct SolveSmem {
   double memo_c[kMemo];
   float memo_B[kMemo];
   int n_memo;
+  float xs[NDIM];   // lane-group kernel: x (+ bτ) staged once; thread 0 derives the pass shift
+  float lg_B;
   double dg[NDIM];  // Dg(x + bτ) for the Laplace proposal (R28)
   float fmax_part[NT / 32];
   double c_next;
@@ -441,15 +443,26 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
   const double sigma_d = sqrt(P.gp.delta_eff * tau);
   const float sigma = (float)sigma_d;
   const float sigma_s = opaque((float)(sigma_d * (double)kBMScale));  // y = x + σz = x + (σC)ẑ
-  float xs[NDIM];
+  // generic kernel: every thread keeps x in registers (the sample loop reads it); lane-group
+  // kernel: each lane loads its own 12 coordinates inside lg_pass, so x is staged once in
+  // shared memory for thread 0's per-pass shift and epilogue (no 3 × n register arrays to spill)
+  float xs[kLG ? 1 : NDIM];
+  if constexpr (kLG) {
+    for (int d = threadIdx.x; d < NDIM; d += NT) {
+      const float xv = P.x[m * NDIM + d];
+      sm.xs[d] = P.drift ? __fadd_rn(xv, __fmul_rn(P.drift[m * NDIM + d], (float)tau)) : xv;
+    }
+    __syncthreads();
+  } else {
 #pragma unroll
-  for (int d = 0; d < NDIM; ++d) {
-    const float xv = P.x[m * NDIM + d];
-    xs[d] = P.drift ? __fadd_rn(xv, __fmul_rn(P.drift[m * NDIM + d], (float)tau)) : xv;
+    for (int d = 0; d < NDIM; ++d) {
+      const float xv = P.x[m * NDIM + d];
+      xs[d] = P.drift ? __fadd_rn(xv, __fmul_rn(P.drift[m * NDIM + d], (float)tau)) : xv;
+    }
   }
 
   if (threadIdx.x == 0) {
-    sm.c_next = unit_prologue<Tgt, NDIM>(P, tgt, m, j, sigma_d, xs, sm.dg);
+    sm.c_next = unit_prologue<Tgt, NDIM>(P, tgt, m, j, sigma_d, kLG ? sm.xs : xs, sm.dg);
     sm.shift = (sigma_d == 0.0) ? 1.f : 0.f;
     sm.n_memo = 0;
   }
@@ -470,32 +483,46 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
     const float A = opaque((float)(-c * kLog2e));
     // Proposal centre (R28): plain → x + bτ; Laplace → μ = x + bτ − cσ²·Dg(x + bτ) (fp32, every
     // thread computes the same values in double); tz = log2-domain tilt per ẑ coordinate.
-    float ctr[NDIM], tz[NDIM];
-    float tilt_max = 0.f;
+    // The lane-group kernel (plain proposal only) has thread 0 derive B and core_ref from the
+    // staged x and broadcast B.
+    float ctr[kLG ? 1 : NDIM], tz[kLG ? 1 : NDIM];
+    float core_ref = 0.f, B;
+    if constexpr (kLG) {
+      if (threadIdx.x == 0) {
+        float z0[NDIM];
 #pragma unroll
-    for (int d = 0; d < NDIM; ++d) {
-      ctr[d] = xs[d];
-      tz[d] = 0.f;
-    }
-    if (P.proposal) {
+        for (int d = 0; d < NDIM; ++d) z0[d] = 0.f;
+        core_ref = tgt.core(sm.xs, 0.f, z0);
+        sm.lg_B = -A * tgt.core_lower(sm.xs, sigma);   // every a_i = A core_i + B ≤ 0
+      }
+      __syncthreads();
+      B = opaque(sm.lg_B);
+    } else {
+      float tilt_max = 0.f;
 #pragma unroll
       for (int d = 0; d < NDIM; ++d) {
-        ctr[d] = (float)((double)xs[d] - c * sigma_d * sigma_d * sm.dg[d]);
-        const double dsh = ((double)ctr[d] - (double)xs[d]) / sigma_d;
-        tz[d] = opaque((float)(-kLog2e * (double)kBMScale * dsh));
-        tilt_max += fabsf(tz[d]);
+        ctr[d] = xs[d];
+        tz[d] = 0.f;
       }
-      tilt_max *= kZmax / kBMScale;  // |ẑ_d| ≤ kZmax / C
-    }
-    float core_ref;
-    {
-      float z0[NDIM];
+      if (P.proposal) {
 #pragma unroll
-      for (int d = 0; d < NDIM; ++d) z0[d] = 0.f;
-      core_ref = tgt.core(ctr, 0.f, z0);
+        for (int d = 0; d < NDIM; ++d) {
+          ctr[d] = (float)((double)xs[d] - c * sigma_d * sigma_d * sm.dg[d]);
+          const double dsh = ((double)ctr[d] - (double)xs[d]) / sigma_d;
+          tz[d] = opaque((float)(-kLog2e * (double)kBMScale * dsh));
+          tilt_max += fabsf(tz[d]);
+        }
+        tilt_max *= kZmax / kBMScale;  // |ẑ_d| ≤ kZmax / C
+      }
+      {
+        float z0[NDIM];
+#pragma unroll
+        for (int d = 0; d < NDIM; ++d) z0[d] = 0.f;
+        core_ref = tgt.core(ctr, 0.f, z0);
+      }
+      // every a_i = A core_i + B (+ tilt) ≤ 0: no weight can overflow
+      B = opaque(-A * tgt.core_lower(ctr, sigma) - tilt_max);
     }
-    // every a_i = A core_i + B (+ tilt) ≤ 0: no weight can overflow
-    float B = opaque(-A * tgt.core_lower(ctr, sigma) - tilt_max);
 
     int hit = -1;  // CTA-uniform: every thread reads the same memo after the last barrier
     if (memo_on)
@@ -573,8 +600,10 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
       }
       bool done = false;
       double dsh[NDIM];
-      if (P.proposal)
-        for (int d = 0; d < NDIM; ++d) dsh[d] = ((double)ctr[d] - (double)xs[d]) / sigma_d;
+      if constexpr (!kLG) {
+        if (P.proposal)
+          for (int d = 0; d < NDIM; ++d) dsh[d] = ((double)ctr[d] - (double)xs[d]) / sigma_d;
+      }
       sm.c_next = pass_epilogue<Tgt, NDIM>(P, tgt, m, j, k, id, c, sigma_d, A, B, core_ref, sums,
                                            P.proposal ? dsh : nullptr, &done);
       sm.shift = done ? 1.f : 0.f;
