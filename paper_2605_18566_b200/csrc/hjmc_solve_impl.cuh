@@ -405,21 +405,24 @@ __device__ __noinline__ double unit_prologue(const SolveParams& P, const Tgt& tg
 #ifndef HJMC_NT
 #define HJMC_NT 256
 #endif
-// Resident CTAs per SM requested from ptxas (caps registers: 4 → 64 regs at 256 threads).
-// Measured on B200: C2 (n = 3) 4/SM beats 3/SM by 2% and 1/SM by 7%; C4 (n = 15) 4/SM beats
-// 2/SM (128 regs, no spill) by 3.3% even with 1.5 spill loads per sample in the loop, and
-// 3/SM by 2%. Above n = 16 the generic path needs z[n] and the moments in registers (1/SM).
+// Resident CTAs per SM requested from ptxas (caps registers: 4 → 64, 3 → 80 at 256 threads).
+// Measured on B200: C2 (n = 3) 4/SM beats 3/SM by 2% and 1/SM by 7%. C4 (n = 15): with the
+// proposal compiled out of the plain kernel (kProp) 3/SM (80 regs, no spill) runs 2% faster
+// than 4/SM (64 regs, spill loads in the sample loop) and 4.7% faster than 2/SM. Above n = 16
+// the generic path needs z[n] and the moments in registers (1/SM).
 #ifndef HJMC_MINB
 #define HJMC_MINB 0
 #endif
 template <int NDIM, bool kLG>
 constexpr int min_blocks() {
-  return HJMC_MINB > 0 ? HJMC_MINB : ((kLG || NDIM <= 16) ? 4 : 1);
+  return HJMC_MINB > 0 ? HJMC_MINB : ((kLG || NDIM <= 6) ? 4 : (NDIM <= 16 ? 3 : 1));
 }
 
 // kLG: the lane-group instantiation (non-antithetic passes of UseLaneGroups targets); it does
 // not contain the generic per-thread path, so its register budget is the lane layout's.
-template <class Tgt, int NDIM, int NT, bool kLG = false>
+// kProp: the Laplace-tilted proposal (R28) is compiled into its own instantiation, so the plain
+// kernels carry no proposal centre / tilt arrays (register pressure at n = 15).
+template <class Tgt, int NDIM, int NT, bool kLG = false, bool kProp = false>
 __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(const __grid_constant__ SolveParams P) {
   __shared__ SolveSmem<NDIM, NT> sm;
   const int64_t unit = blockIdx.x;
@@ -504,7 +507,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         ctr[d] = xs[d];
         tz[d] = 0.f;
       }
-      if (P.proposal) {
+      if constexpr (kProp) {
 #pragma unroll
         for (int d = 0; d < NDIM; ++d) {
           ctr[d] = (float)((double)xs[d] - c * sigma_d * sigma_d * sm.dg[d]);
@@ -538,12 +541,8 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         lg_reduce<NDIM, NT>(sm, S, Mb);
       } else {
         float S, Mz[NDIM];
-        if (P.proposal)
-          mc_accumulate<Tgt, NDIM, NT, true>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base, id,
-                                             P.tag, P.rk, S, Mz, tz);
-        else
-          mc_accumulate<Tgt, NDIM, NT, false>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
-                                              id, P.tag, P.rk, S, Mz, tz);
+        mc_accumulate<Tgt, NDIM, NT, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base, id,
+                                            P.tag, P.rk, S, Mz, tz);
         cta_reduce<NDIM, NT>(sm, S, Mz);
       }
       if (!(sm.sum[0] >= (double)kUnderflowS)) {
@@ -573,12 +572,8 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
           lg_reduce<NDIM, NT>(sm, S, Mb);
         } else {
           float S, Mz[NDIM];
-          if (P.proposal)
-            mc_accumulate<Tgt, NDIM, NT, true>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
-                                               id, P.tag, P.rk, S, Mz, tz);
-          else
-            mc_accumulate<Tgt, NDIM, NT, false>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
-                                                id, P.tag, P.rk, S, Mz, tz);
+          mc_accumulate<Tgt, NDIM, NT, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
+                                              id, P.tag, P.rk, S, Mz, tz);
           cta_reduce<NDIM, NT>(sm, S, Mz);
         }
       }
@@ -600,12 +595,11 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
       }
       bool done = false;
       double dsh[NDIM];
-      if constexpr (!kLG) {
-        if (P.proposal)
-          for (int d = 0; d < NDIM; ++d) dsh[d] = ((double)ctr[d] - (double)xs[d]) / sigma_d;
+      if constexpr (kProp) {
+        for (int d = 0; d < NDIM; ++d) dsh[d] = ((double)ctr[d] - (double)xs[d]) / sigma_d;
       }
       sm.c_next = pass_epilogue<Tgt, NDIM>(P, tgt, m, j, k, id, c, sigma_d, A, B, core_ref, sums,
-                                           P.proposal ? dsh : nullptr, &done);
+                                           kProp ? dsh : nullptr, &done);
       sm.shift = done ? 1.f : 0.f;
     }
     __syncthreads();
@@ -623,11 +617,14 @@ cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
   if (units > 0x7FFFFFFFLL) return cudaErrorInvalidValue;
   if constexpr (UseLaneGroups<Tgt, NDIM>::value) {
     if (!p.antithetic && !p.proposal) {
-      solve_kernel<Tgt, NDIM, NT, true><<<(unsigned)units, NT, 0, s>>>(p);
+      solve_kernel<Tgt, NDIM, NT, true, false><<<(unsigned)units, NT, 0, s>>>(p);
       return cudaGetLastError();
     }
   }
-  solve_kernel<Tgt, NDIM, NT, false><<<(unsigned)units, NT, 0, s>>>(p);
+  if (p.proposal)
+    solve_kernel<Tgt, NDIM, NT, false, true><<<(unsigned)units, NT, 0, s>>>(p);
+  else
+    solve_kernel<Tgt, NDIM, NT, false, false><<<(unsigned)units, NT, 0, s>>>(p);
   return cudaGetLastError();
 }
 
