@@ -81,6 +81,16 @@ def test_create_validation_without_gpu(lib):
     cc = _lib.Config.from_buffer_copy(c)
     cc.c_min, cc.c_max = 5.0, 1.0
     assert lib.hjmc_create(C.byref(cc), C.byref(h)) == _lib.HJMC_EINVAL
+    cc = _lib.Config.from_buffer_copy(c)
+    cc.flags = 8                                   # no such flag bit
+    assert lib.hjmc_create(C.byref(cc), C.byref(h)) == _lib.HJMC_EINVAL
+    # every declared flag passes validation (then needs a device)
+    cc.flags = _lib.FLAG_SYNC_CHECK | _lib.FLAG_SKIP_STATIONARY | _lib.FLAG_REUSE_PASSES
+    rcf = lib.hjmc_create(C.byref(cc), C.byref(h))
+    assert rcf != _lib.HJMC_EINVAL
+    if h.value:
+        lib.hjmc_destroy(h)
+        h = C.c_void_p()
     rc = lib.hjmc_create(C.byref(c), C.byref(h))
     import torch
 
