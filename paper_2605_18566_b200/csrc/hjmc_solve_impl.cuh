@@ -207,17 +207,27 @@ struct UseLaneGroups {
                                 NDIM <= 48;
 };
 
+#ifndef HJMC_LG_LANES
+#define HJMC_LG_LANES 4
+#endif
+// Lanes per sample (4 or 2) and what each lane owns: kLgSpan = 48 / lanes coordinates
+// (a multiple of lcm(3, 4) = 12), i.e. kLgSpan / 4 Philox blocks and kLgSpan / 3 (x, y, θ) pairs.
+constexpr int kLgLanes = HJMC_LG_LANES;
+constexpr int kLgSpan = 48 / kLgLanes;
+static_assert(kLgLanes == 2 || kLgLanes == 4, "lane groups of 2 or 4");
+
 template <int NDIM, int NT, bool kMaxMode>
 __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float tau, float sigma_s,
                                         float A, float B, uint32_t w1base, uint32_t qid,
-                                        float& S, float (&Mb)[12], float& amax) {
-  const int lane = threadIdx.x & 31, l = lane & 3;
-  const uint32_t slot = (threadIdx.x >> 5) * 8 + (lane >> 2);   // sample slot in the CTA
-  constexpr uint32_t kStride = NT / 4;
-  float xb[12];
+                                        float& S, float (&Mb)[kLgSpan], float& amax) {
+  constexpr int kBlocks = kLgSpan / 4, kTriples = kLgSpan / 3;
+  const int lane = threadIdx.x & 31, l = lane & (kLgLanes - 1);
+  const uint32_t slot = (threadIdx.x >> 5) * (32 / kLgLanes) + (lane / kLgLanes);  // sample slot
+  constexpr uint32_t kStride = NT / kLgLanes;
+  float xb[kLgSpan];
 #pragma unroll
-  for (int c = 0; c < 12; ++c) {
-    const int d = 12 * l + c;
+  for (int c = 0; c < kLgSpan; ++c) {
+    const int d = kLgSpan * l + c;
     float xv = 0.f;
     if (d < NDIM) {
       xv = P.x[m * NDIM + d];
@@ -228,28 +238,28 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
   S = 0.f;
   amax = -3.0e38f;
 #pragma unroll
-  for (int c = 0; c < 12; ++c) Mb[c] = 0.f;
+  for (int c = 0; c < kLgSpan; ++c) Mb[c] = 0.f;
   const uint32_t N = P.N;
   // One sample per lane group per trip; trips where every slot's sample exists run without
   // the i < N guard (C5: N = 2^20, all of them), the ragged last trip with it.
   auto trip = [&](uint32_t i, bool guard) {
-    float z[12];
+    float z[kLgSpan];
 #pragma unroll
-    for (int qd = 0; qd < 3; ++qd) {
-      const uint4 w = philox4x32_10(i, w1base | (uint32_t)(3 * l + qd), qid, P.tag, P.rk);
+    for (int qd = 0; qd < kBlocks; ++qd) {
+      const uint4 w = philox4x32_10(i, w1base | (uint32_t)(kBlocks * l + qd), qid, P.tag, P.rk);
       box_muller_hat<true>(w.x, w.y, z[4 * qd], z[4 * qd + 1]);
       box_muller_hat<true>(w.z, w.w, z[4 * qd + 2], z[4 * qd + 3]);
     }
     float best = 3.0e38f;
 #pragma unroll
-    for (int pq = 0; pq < 4; ++pq) {
+    for (int pq = 0; pq < kTriples; ++pq) {
       const float a = fmaf(sigma_s, z[3 * pq], xb[3 * pq]);
       const float b = fmaf(sigma_s, z[3 * pq + 1], xb[3 * pq + 1]);
       const float r2 = fmaf(a, a, b * b);
-      best = (12 * l + 3 * pq + 1 < NDIM) ? fminf(best, r2) : best;
+      best = (kLgSpan * l + 3 * pq + 1 < NDIM) ? fminf(best, r2) : best;
     }
-    best = fminf(best, __shfl_xor_sync(0xffffffffu, best, 1));
-    best = fminf(best, __shfl_xor_sync(0xffffffffu, best, 2));
+#pragma unroll
+    for (int o = 1; o < kLgLanes; o <<= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
     const float core = sqrt_approx(best);
     if (!guard || i < N) {
       if (kMaxMode) {
@@ -258,7 +268,7 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
         const float wt = ex2_approx(fmaf(A, core, B));
         S += wt;
 #pragma unroll
-        for (int c = 0; c < 12; ++c) Mb[c] = fmaf(wt, z[c], Mb[c]);
+        for (int c = 0; c < kLgSpan; ++c) Mb[c] = fmaf(wt, z[c], Mb[c]);
       }
     }
   };
@@ -270,19 +280,19 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
 
 // Merge the lane-group sums into sm.sum (double), deterministic order.
 template <int NDIM, int NT>
-__device__ __forceinline__ void lg_reduce(SolveSmem<NDIM, NT>& sm, float S, float (&Mb)[12]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, l = lane & 3;
+__device__ __forceinline__ void lg_reduce(SolveSmem<NDIM, NT>& sm, float S, float (&Mb)[kLgSpan]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, l = lane & (kLgLanes - 1);
 #pragma unroll
-  for (int o = 4; o < 32; o <<= 1) {           // sum over the warp's 8 lane groups
+  for (int o = kLgLanes; o < 32; o <<= 1) {      // sum over the warp's lane groups
     S += __shfl_xor_sync(0xffffffffu, S, o);
 #pragma unroll
-    for (int c = 0; c < 12; ++c) Mb[c] += __shfl_xor_sync(0xffffffffu, Mb[c], o);
+    for (int c = 0; c < kLgSpan; ++c) Mb[c] += __shfl_xor_sync(0xffffffffu, Mb[c], o);
   }
-  if (lane < 4) {
+  if (lane < kLgLanes) {
     if (l == 0) sm.part[warp][0] = S;
 #pragma unroll
-    for (int c = 0; c < 12; ++c)
-      if (12 * l + c < NDIM) sm.part[warp][1 + 12 * l + c] = Mb[c];
+    for (int c = 0; c < kLgSpan; ++c)
+      if (kLgSpan * l + c < NDIM) sm.part[warp][1 + kLgSpan * l + c] = Mb[c];
   }
   __syncthreads();
   for (int col = threadIdx.x; col < NDIM + 1; col += NT) {
@@ -415,7 +425,9 @@ __device__ __noinline__ double unit_prologue(const SolveParams& P, const Tgt& tg
 #endif
 template <int NDIM, bool kLG>
 constexpr int min_blocks() {
-  return HJMC_MINB > 0 ? HJMC_MINB : ((kLG || NDIM <= 6) ? 4 : (NDIM <= 16 ? 3 : 1));
+  if (HJMC_MINB > 0) return HJMC_MINB;
+  if (kLG) return kLgLanes == 4 ? 4 : 2;          // 2-lane groups hold 24 + 24 + 16 floats
+  return NDIM <= 6 ? 4 : (NDIM <= 16 ? 3 : 1);
 }
 
 // kLG: the lane-group instantiation (non-antithetic passes of UseLaneGroups targets); it does
@@ -536,7 +548,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         }
     if (hit < 0) {
       if constexpr (kLG) {
-        float S, Mb[12], amax;
+        float S, Mb[kLgSpan], amax;
         lg_pass<NDIM, NT, false>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax);
         lg_reduce<NDIM, NT>(sm, S, Mb);
       } else {
@@ -550,7 +562,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         // the exact maximum exponent, the plain two-pass log-sum-exp.
         float amax_t;
         if constexpr (kLG) {
-          float S, Mb[12];
+          float S, Mb[kLgSpan];
           lg_pass<NDIM, NT, true>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax_t);
         } else {
           amax_t = mc_max_exponent<Tgt, NDIM, NT>(tgt, ctr, sigma_s, A, P.N, P.antithetic, w1base,
@@ -567,7 +579,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         __syncthreads();
         B = -sm.shift;
         if constexpr (kLG) {
-          float S, Mb[12], am;
+          float S, Mb[kLgSpan], am;
           lg_pass<NDIM, NT, false>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, am);
           lg_reduce<NDIM, NT>(sm, S, Mb);
         } else {

@@ -13,6 +13,8 @@ VARIANTS = {
     "lgu2": ["-DHJMC_LG_UNROLL=2"],
     "mb3": ["-DHJMC_MINB=3"],
     "mb4": ["-DHJMC_MINB=4"],
+    "lg4": ["-DHJMC_LG_LANES=4"],
+    "lg2": ["-DHJMC_LG_LANES=2"],
 }
 
 if __name__ == "__main__":
