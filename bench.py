@@ -340,6 +340,17 @@ def run_ours(args):
                    "peak_gbps": hbm_peak,
                    "frac": (hbm_gbps / hbm_peak) if hbm_peak else None,
                    "note": "no sample touches HBM; the streams are queries and per-iterate results"}
+    # context for the fraction: the measured throughput ceiling of this kernel's own instruction
+    # mix (tools/mix_ceiling.cu, C2 only)
+    mix_file = os.path.join(ROOT, "profiles", "r1_mix_ceiling.json")
+    if preset.name == "c2_dubins_n3" and os.path.exists(mix_file):
+        with open(mix_file) as fh:
+            mix = json.load(fh)["mixes"]["full_c2_mix"]["evals_per_clk_per_sm"]
+        f_hz = (clk["sm_mhz"] if clk and clk.get("sm_mhz") else RL.F_MAX_MHZ) * 1e6
+        per_clk = evals_step_rank / (kern_avg_ms / 1000.0) / (RL.NSM * f_hz)
+        roof["mix_ceiling"] = {"evals_per_clk_per_sm": mix, "kernel_evals_per_clk_per_sm": per_clk,
+                               "frac": per_clk / mix,
+                               "source": "profiles/r1_mix_ceiling.json (synthetic same-mix kernel)"}
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
