@@ -127,16 +127,28 @@ class Solver:
             a = t.as_tensor(np.asarray(a), dtype=dtype, device=self.device)
         return a.contiguous()
 
+    def _as_query(self, x):
+        x = self._as_dev(x)
+        if x.dim() != 2 or x.shape[1] != self.cfg.n:
+            raise ValueError(f"queries must have shape (M, {self.cfg.n}), got {tuple(x.shape)}")
+        return x
+
     # -- entry points ------------------------------------------------------------------------
     def value_grad(self, x, c, tau: float, j_tag: int = 1, k_tag: int = 0, qid_base: int = 0,
                    qid=None, drift=None, want_dv: bool = True):
         """One Φ pass at frozen per-query c (hjmc_value_grad). Returns (v[M], dv[M][n])."""
         t = self.torch
-        x = self._as_dev(x)
+        x = self._as_query(x)
         M = x.shape[0]
         c = self._as_dev(c) if c is not None else None
+        if c is not None and tuple(c.shape) != (M,):
+            raise ValueError(f"c must have shape ({M},), got {tuple(c.shape)}")
         drift = self._as_dev(drift) if drift is not None else None
+        if drift is not None and tuple(drift.shape) != tuple(x.shape):
+            raise ValueError(f"drift must have the queries' shape {tuple(x.shape)}")
         q = self._as_dev(qid, t.int32) if qid is not None else None
+        if q is not None and tuple(q.shape) != (M,):
+            raise ValueError(f"qid must have shape ({M},), got {tuple(q.shape)}")
         v = t.empty(M, device=self.device)
         dv = t.empty((M, self.cfg.n), device=self.device) if want_dv else None
         self._check(self.L.hjmc_value_grad(self.h, _ptr(x), _ptr(c), _ptr(q), qid_base, M,
@@ -153,14 +165,40 @@ class Solver:
             r["chist"] = e(K, Kp, M)
         return r
 
+    def _shapes(self, M: int) -> dict:
+        n, K, Kp = self.cfg.n, self.cfg.K, self.cfg.Kp
+        return {"v": (M,), "dv": (M, n), "c": (M,), "tube": (M,), "g0": (M,),
+                "vhist": (K, Kp, M), "chist": (K, Kp, M)}
+
+    def _check_out(self, out: dict, M: int):
+        """Caller-provided output buffers: the C-ABI writes through raw pointers, so shape,
+        dtype, device and contiguity are checked here rather than trusted."""
+        t = self.torch
+        for k, shape in self._shapes(M).items():
+            a = out.get(k)
+            if a is None:
+                continue
+            if (tuple(a.shape) != shape or a.dtype != t.float32 or a.device != self.device
+                    or not a.is_contiguous()):
+                raise ValueError(f"out[{k!r}] must be a contiguous float32 tensor of shape "
+                                 f"{shape} on {self.device}, got {tuple(a.shape)} {a.dtype} "
+                                 f"{a.device}")
+
     def solve_slice(self, x, qid_base: int = 0, qid=None, drift=None, out=None, hist: bool = True):
         """Algorithm 1 over all horizons + tube (hjmc_solve_slice). Returns a dict of tensors."""
         t = self.torch
-        x = self._as_dev(x)
+        x = self._as_query(x)
         M = x.shape[0]
         drift = self._as_dev(drift) if drift is not None else None
+        if drift is not None and tuple(drift.shape) != tuple(x.shape):
+            raise ValueError(f"drift must have the queries' shape {tuple(x.shape)}")
         q = self._as_dev(qid, t.int32) if qid is not None else None
-        out = out if out is not None else self.alloc_result(M, hist)
+        if q is not None and tuple(q.shape) != (M,):
+            raise ValueError(f"qid must have shape ({M},), got {tuple(q.shape)}")
+        if out is None:
+            out = self.alloc_result(M, hist)
+        else:
+            self._check_out(out, M)
         res = _lib.Result(*[C.c_void_p(out[k].data_ptr()) if out.get(k) is not None else None
                             for k in ("v", "dv", "c", "tube", "vhist", "chist", "g0")])
         self._check(self.L.hjmc_solve_slice(self.h, _ptr(x), _ptr(q), qid_base, M, _ptr(drift),

@@ -541,3 +541,22 @@ def test_laplace_proposal_solve_slice(O):
     s, P = pair(O, n=3, delta=0.01, T=1.0, K=2, Kp=3, N=2500, system="dubins_rel",
                 target="disk", tgt_params=(5.0,), proposal="laplace")
     _compare_solve(O, s, P, _grid(-12, 12, 7, 3, (0, 0, math.pi / 2)), qid_base=3)
+
+
+def test_binding_validates_shapes():
+    """The C-ABI writes through raw pointers, so the binding rejects mis-shaped buffers."""
+    s = Solver(SolverConfig.from_preset(I.C2, N=256, K=2, Kp=2))
+    x = I.queries(I.C2)[:10]
+    with pytest.raises(ValueError):
+        s.solve_slice(x[:, :2])                                    # wrong n
+    out = s.alloc_result(10)
+    out["vhist"] = torch.empty(2, 2, 9, device="cuda")            # wrong M
+    with pytest.raises(ValueError):
+        s.solve_slice(x, out=out)
+    with pytest.raises(ValueError):
+        s.value_grad(x, np.ones(9, np.float32), 0.5)               # c of the wrong length
+    with pytest.raises(ValueError):
+        s.solve_slice(x, qid=np.arange(11, dtype=np.int32))
+    with pytest.raises(ValueError):
+        s.solve_slice(x, drift=np.zeros((10, 2), np.float32))
+    s.solve_slice(x, out=s.alloc_result(10))                        # the right shapes pass
