@@ -105,7 +105,12 @@ __global__ void __launch_bounds__(256, 4) mix(float* out, Stamp* st, uint32_t k0
 // Parametric variant for pricing alternatives: the Philox integer share as above, kM MUFU
 // (cycling LG2, SQRT, COS, EX2) and kF dependent FFMAs per eval — e.g. (8, 14) ≈ today's C2
 // mix, (7, 24) ≈ one MUFU traded for a 10-FFMA polynomial, (6, 34), (5, 44).
-template <int kM, int kF>
+__device__ __forceinline__ void mulsplit(uint32_t a, uint32_t m, uint32_t& hi, uint32_t& lo) {
+  asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(a), "r"(m));
+  asm volatile("mad.lo.u32 %0, %1, %2, 0x9E3779B9;" : "=r"(lo) : "r"(a), "r"(m));
+}
+
+template <int kM, int kF, bool kSplit = false>
 __global__ void __launch_bounds__(256, 4) pmix(float* out, Stamp* st, uint32_t k0, float p1) {
   uint32_t u[kChains], w[kChains];
   float f[kChains];
@@ -123,8 +128,13 @@ __global__ void __launch_bounds__(256, 4) pmix(float* out, Stamp* st, uint32_t k
 #pragma unroll
       for (int r = 0; r < 6; ++r) {
         uint32_t h0, l0, h1, l1;
-        mulw(u[c], 0xD2511F53u, h0, l0);
-        mulw(w[c], 0xCD9E8D57u, h1, l1);
+        if (kSplit) {
+          mulsplit(u[c], 0xD2511F53u, h0, l0);
+          mulsplit(w[c], 0xCD9E8D57u, h1, l1);
+        } else {
+          mulw(u[c], 0xD2511F53u, h0, l0);
+          mulw(w[c], 0xCD9E8D57u, h1, l1);
+        }
         u[c] = h1 ^ l0 ^ (k0 + r);
         w[c] = h0 ^ l1 ^ (k0 * 3u + r);
       }
@@ -203,6 +213,9 @@ int main() {
   r.push_back({"p_int+6mufu+34ffma", run(pmix<6, 34>, nsm), 6});
   r.push_back({"p_int+5mufu+44ffma", run(pmix<5, 44>, nsm), 5});
   r.push_back({"p_int+8mufu+30ffma", run(pmix<8, 30>, nsm), 8});
+  r.push_back({"p_splitmul+8mufu+14ffma", run(pmix<8, 14, true>, nsm), 8});
+  r.push_back({"p_int+0mufu+14ffma", run(pmix<0, 14>, nsm), 0});
+  r.push_back({"p_splitmul+0mufu+14ffma", run(pmix<0, 14, true>, nsm), 0});
   if (cudaGetLastError() != cudaSuccess) return 1;
   printf("{\n  \"what\": \"synthetic C2 instruction mix per eval: 8 MUFU, 12 IMAD.WIDE + 16 LOP3, ~14 FP32; "
          "evals per SM clock (median over SMs) and MUFU lane-ops/clk/SM (peak 16)\",\n  \"mixes\": {\n");
