@@ -26,11 +26,15 @@ namespace hjmc {
 #ifndef HJMC_LG_UNROLL
 #define HJMC_LG_UNROLL 2
 #endif
+#ifndef HJMC_GROUP_UNROLL
+#define HJMC_GROUP_UNROLL 2
+#endif
 
 namespace {
 
 constexpr int kSampleUnroll = HJMC_UNROLL;
 constexpr int kLgUnroll = HJMC_LG_UNROLL;
+constexpr int kGroupUnroll = HJMC_GROUP_UNROLL;  // draw groups per trip when G > 1
 constexpr double kLog2e = 1.4426950408889634074;
 constexpr double kLn2 = 0.69314718055994530942;
 constexpr float kUnderflowS = 7.888609052210118e-31f;  // 2^-100: fallback threshold
@@ -87,7 +91,7 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
   const uint32_t groups = (draws + L::G - 1) / L::G;
   if (!antithetic) {
     const uint32_t full = N / L::G;  // groups whose G samples all exist: no per-sample guard
-#pragma unroll(L::G == 1 ? kSampleUnroll : 1)
+#pragma unroll(L::G == 1 ? kSampleUnroll : kGroupUnroll)
     for (uint32_t g = threadIdx.x; g < full; g += NT) {
       float zz[L::L];
       group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);

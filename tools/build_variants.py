@@ -15,6 +15,8 @@ VARIANTS = {
     "mb4": ["-DHJMC_MINB=4"],
     "lg4": ["-DHJMC_LG_LANES=4"],
     "lg2": ["-DHJMC_LG_LANES=2"],
+    "gu1": ["-DHJMC_GROUP_UNROLL=1"],
+    "gu2": ["-DHJMC_GROUP_UNROLL=2"],
 }
 
 if __name__ == "__main__":
