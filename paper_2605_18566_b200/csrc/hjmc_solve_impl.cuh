@@ -77,12 +77,15 @@ __device__ __forceinline__ void accumulate_sample(const Tgt& tgt, const float (&
   for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(sw, z[d], Mz[d]);
 }
 
+// NT here is the size of the thread group that shares one unit (the CTA, or one warp in the
+// warp-per-unit kernel) and tid the thread's index in it.
 template <class Tgt, int NDIM, int NT, bool kTilt = false>
 __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[NDIM],
                                                    float sigma, float A, float B, uint32_t N,
                                                    int antithetic, uint32_t w1base, uint32_t qid,
                                                    uint32_t tag, const RoundKeys& rk, float& S,
-                                                   float (&Mz)[NDIM], const float (&tz)[NDIM]) {
+                                                   float (&Mz)[NDIM], const float (&tz)[NDIM],
+                                                   uint32_t tid) {
   using L = DrawLayout<NDIM>;
   S = 0.f;
 #pragma unroll
@@ -92,14 +95,14 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
   if (!antithetic) {
     const uint32_t full = N / L::G;  // groups whose G samples all exist: no per-sample guard
 #pragma unroll(L::G == 1 ? kSampleUnroll : kGroupUnroll)
-    for (uint32_t g = threadIdx.x; g < full; g += NT) {
+    for (uint32_t g = tid; g < full; g += NT) {
       float zz[L::L];
       group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
 #pragma unroll
       for (int r = 0; r < L::G; ++r)
         accumulate_sample<Tgt, NDIM, kTilt>(tgt, xs, sigma, A, B, tz, zz + r * NDIM, 1.f, S, Mz);
     }
-    for (uint32_t g = full + threadIdx.x; g < groups; g += NT) {  // ragged tail group
+    for (uint32_t g = full + tid; g < groups; g += NT) {  // ragged tail group
       float zz[L::L];
       group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
 #pragma unroll
@@ -108,7 +111,7 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
           accumulate_sample<Tgt, NDIM, kTilt>(tgt, xs, sigma, A, B, tz, zz + r * NDIM, 1.f, S, Mz);
     }
   } else {
-    for (uint32_t g = threadIdx.x; g < groups; g += NT) {
+    for (uint32_t g = tid; g < groups; g += NT) {
       float zz[L::L];
       group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
 #pragma unroll
@@ -128,12 +131,13 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
 template <class Tgt, int NDIM, int NT>
 __device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float sigma, float A,
                                  uint32_t N, int antithetic, uint32_t w1base, uint32_t qid,
-                                 uint32_t tag, const RoundKeys& rk, const float (&tz)[NDIM]) {
+                                 uint32_t tag, const RoundKeys& rk, const float (&tz)[NDIM],
+                                 uint32_t tid) {
   using L = DrawLayout<NDIM>;
   float amax = -3.0e38f;
   const uint32_t draws = antithetic ? (N >> 1) + (N & 1u) : N;
   const uint32_t groups = (draws + L::G - 1) / L::G;
-  for (uint32_t g = threadIdx.x; g < groups; g += NT) {
+  for (uint32_t g = tid; g < groups; g += NT) {
     float zz[L::L];
     group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
 #pragma unroll
@@ -176,20 +180,31 @@ struct SolveSmem {
   float shift;
 };
 
-// CTA-wide merge of (S, Mz[NDIM]) into sm.sum (double), deterministic order.
+// Group-wide merge of (S, Mz[NDIM]) into sm.sum (double), deterministic order. NT = group
+// size: the CTA (shared-memory merge across its warps) or one warp (shuffles only).
 template <int NDIM, int NT>
-__device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, float (&Mz)[NDIM]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, float (&Mz)[NDIM],
+                                           uint32_t tid) {
+  const int lane = tid & 31, warp = tid >> 5;
   S = warp_sum(S);
 #pragma unroll
   for (int d = 0; d < NDIM; ++d) Mz[d] = warp_sum(Mz[d]);
+  if constexpr (NT == 32) {
+    if (lane == 0) {
+      sm.sum[0] = (double)S;
+#pragma unroll
+      for (int d = 0; d < NDIM; ++d) sm.sum[1 + d] = (double)Mz[d];
+    }
+    __syncwarp();
+    return;
+  }
   if (lane == 0) {
     sm.part[warp][0] = S;
 #pragma unroll
     for (int d = 0; d < NDIM; ++d) sm.part[warp][1 + d] = Mz[d];
   }
   __syncthreads();
-  for (int col = threadIdx.x; col < NDIM + 1; col += NT) {
+  for (int col = tid; col < NDIM + 1; col += NT) {
     double acc = 0.0;
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) acc += (double)sm.part[w][col];
@@ -438,10 +453,27 @@ constexpr int min_blocks() {
 // not contain the generic per-thread path, so its register budget is the lane layout's.
 // kProp: the Laplace-tilted proposal (R28) is compiled into its own instantiation, so the plain
 // kernels carry no proposal centre / tilt arrays (register pressure at n = 15).
-template <class Tgt, int NDIM, int NT, bool kLG = false, bool kProp = false>
+// GS: threads per unit — the whole CTA (GS = NT), or one warp (GS = 32: the warp-per-unit
+// kernel for small N, where a CTA-wide unit would spend most of its time in the per-pass
+// reduction, barriers and thread-0 epilogue; with one unit per warp those latencies of one
+// unit overlap the sampling of the CTA's other seven, and no __syncthreads exists).
+template <class Tgt, int NDIM, int NT, bool kLG = false, bool kProp = false, int GS = NT>
 __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(const __grid_constant__ SolveParams P) {
-  __shared__ SolveSmem<NDIM, NT> sm;
-  const int64_t unit = blockIdx.x;
+  static_assert(GS == NT || (GS == 32 && !kLG), "warp-per-unit only for the generic kernel");
+  __shared__ SolveSmem<NDIM, GS> smv[NT / GS];
+  SolveSmem<NDIM, GS>& sm = smv[threadIdx.x / GS];
+  const uint32_t tid = threadIdx.x % GS;
+  auto gsync = [] {
+    if constexpr (GS == NT) __syncthreads();
+    else __syncwarp();
+  };
+  const int64_t unit = (int64_t)blockIdx.x * (NT / GS) + threadIdx.x / GS;
+  if constexpr (GS != NT) {
+    const int64_t units = (P.mode == kModeSolve)  ? P.M * (int64_t)P.K
+                          : (P.mode == kModePass) ? P.M * (int64_t)P.n_active
+                                                  : P.M;
+    if (unit >= units) return;  // whole warp: the last CTA's spare warps
+  }
   int64_t m;
   int j;
   if (P.mode == kModeSolve) {
@@ -480,15 +512,15 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
     }
   }
 
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     sm.c_next = unit_prologue<Tgt, NDIM>(P, tgt, m, j, sigma_d, kLG ? sm.xs : xs, sm.dg);
     sm.shift = (sigma_d == 0.0) ? 1.f : 0.f;
     sm.n_memo = 0;
   }
-  __syncthreads();
+  gsync();
   double c = sm.c_next;
   if (sm.shift != 0.f) return;  // σ = 0: handled by the prologue (uniform branch)
-  __syncthreads();
+  gsync();
 
   const uint32_t jw = (P.mode != kModeValueGrad) ? (uint32_t)j : P.jtag;
   unsigned passes = 0;  // Φ passes this unit executed (thread 0)
@@ -507,7 +539,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
     float ctr[kLG ? 1 : NDIM], tz[kLG ? 1 : NDIM];
     float core_ref = 0.f, B;
     if constexpr (kLG) {
-      if (threadIdx.x == 0) {
+      if (tid == 0) {
         float z0[NDIM];
 #pragma unroll
         for (int d = 0; d < NDIM; ++d) z0[d] = 0.f;
@@ -557,9 +589,9 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         lg_reduce<NDIM, NT>(sm, S, Mb);
       } else {
         float S, Mz[NDIM];
-        mc_accumulate<Tgt, NDIM, NT, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base, id,
-                                            P.tag, P.rk, S, Mz, tz);
-        cta_reduce<NDIM, NT>(sm, S, Mz);
+        mc_accumulate<Tgt, NDIM, GS, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base, id,
+                                            P.tag, P.rk, S, Mz, tz, tid);
+        cta_reduce<NDIM, GS>(sm, S, Mz, tid);
       }
       if (!(sm.sum[0] >= (double)kUnderflowS)) {
         // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with
@@ -569,18 +601,18 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
           float S, Mb[kLgSpan];
           lg_pass<NDIM, NT, true>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax_t);
         } else {
-          amax_t = mc_max_exponent<Tgt, NDIM, NT>(tgt, ctr, sigma_s, A, P.N, P.antithetic, w1base,
-                                                  id, P.tag, P.rk, tz);
+          amax_t = mc_max_exponent<Tgt, NDIM, GS>(tgt, ctr, sigma_s, A, P.N, P.antithetic, w1base,
+                                                  id, P.tag, P.rk, tz, tid);
         }
         const float amax = warp_max(amax_t);
-        if ((threadIdx.x & 31) == 0) sm.fmax_part[threadIdx.x >> 5] = amax;
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        if ((tid & 31) == 0) sm.fmax_part[tid >> 5] = amax;
+        gsync();
+        if (tid == 0) {
           float mx = sm.fmax_part[0];
-          for (int w = 1; w < NT / 32; ++w) mx = fmaxf(mx, sm.fmax_part[w]);
+          for (int w = 1; w < GS / 32; ++w) mx = fmaxf(mx, sm.fmax_part[w]);
           sm.shift = mx;
         }
-        __syncthreads();
+        gsync();
         B = -sm.shift;
         if constexpr (kLG) {
           float S, Mb[kLgSpan], am;
@@ -588,13 +620,13 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
           lg_reduce<NDIM, NT>(sm, S, Mb);
         } else {
           float S, Mz[NDIM];
-          mc_accumulate<Tgt, NDIM, NT, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
-                                              id, P.tag, P.rk, S, Mz, tz);
-          cta_reduce<NDIM, NT>(sm, S, Mz);
+          mc_accumulate<Tgt, NDIM, GS, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
+                                              id, P.tag, P.rk, S, Mz, tz, tid);
+          cta_reduce<NDIM, GS>(sm, S, Mz, tid);
         }
       }
     }  // hit < 0
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       const double* sums = sm.sum;
       if (hit >= 0) {
         sums = sm.memo_sum[hit];
@@ -618,14 +650,21 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
                                            kProp ? dsh : nullptr, &done);
       sm.shift = done ? 1.f : 0.f;
     }
-    __syncthreads();
+    gsync();
     c = sm.c_next;
     const bool done = sm.shift != 0.f;
-    __syncthreads();
+    gsync();
     if (done) break;
   }
-  if (threadIdx.x == 0 && P.passes) atomicAdd(P.passes, (unsigned long long)passes);
+  if (tid == 0 && P.passes) atomicAdd(P.passes, (unsigned long long)passes);
 }
+
+// Plain passes with at most this many samples run one unit per warp (GS = 32) instead of one
+// per CTA: measured on B200.
+#ifndef HJMC_WARP_UNIT_MAX_N
+#define HJMC_WARP_UNIT_MAX_N 32768
+#endif
+constexpr uint32_t kWarpUnitMaxN = HJMC_WARP_UNIT_MAX_N;
 
 template <class Tgt, int NDIM, int NT>
 cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
@@ -637,10 +676,15 @@ cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
       return cudaGetLastError();
     }
   }
-  if (p.proposal)
+  if (p.proposal) {
     solve_kernel<Tgt, NDIM, NT, false, true><<<(unsigned)units, NT, 0, s>>>(p);
-  else
+  } else if (p.N <= kWarpUnitMaxN) {
+    constexpr int kPerCta = NT / 32;
+    const int64_t ctas = (units + kPerCta - 1) / kPerCta;
+    solve_kernel<Tgt, NDIM, NT, false, false, 32><<<(unsigned)ctas, NT, 0, s>>>(p);
+  } else {
     solve_kernel<Tgt, NDIM, NT, false, false><<<(unsigned)units, NT, 0, s>>>(p);
+  }
   return cudaGetLastError();
 }
 

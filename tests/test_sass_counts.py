@@ -56,9 +56,9 @@ def hot_loop_counts(funcs, pattern, n=None):
 
 
 @pytest.mark.parametrize("pattern,n,target", [
-    ("DiskILi3EEELi3ELi256ELb0", 3, "disk"),
-    ("RelDisk6ILi6EEELi6ELi256ELb0", 6, "rel_disk6"),
-    ("PairUnionILi15EEELi15ELi256ELb0", 15, "pair_union"),
+    ("DiskILi3EEELi3ELi256ELb0ELb0ELi256E", 3, "disk"),
+    ("RelDisk6ILi6EEELi6ELi256ELb0ELb0ELi256E", 6, "rel_disk6"),
+    ("PairUnionILi15EEELi15ELi256ELb0ELb0ELi256E", 15, "pair_union"),
 ])
 def test_generic_kernels_execute_the_minimal_philox_work(funcs, pattern, n, target):
     from paper_2605_18566_b200 import roofline as RL

@@ -17,6 +17,8 @@ VARIANTS = {
     "lg2": ["-DHJMC_LG_LANES=2"],
     "gu1": ["-DHJMC_GROUP_UNROLL=1"],
     "gu2": ["-DHJMC_GROUP_UNROLL=2"],
+    "wu0": ["-DHJMC_WARP_UNIT_MAX_N=0"],
+    "wu64k": ["-DHJMC_WARP_UNIT_MAX_N=65536"],
 }
 
 if __name__ == "__main__":
