@@ -560,3 +560,13 @@ def test_binding_validates_shapes():
     with pytest.raises(ValueError):
         s.solve_slice(x, drift=np.zeros((10, 2), np.float32))
     s.solve_slice(x, out=s.alloc_result(10))                        # the right shapes pass
+
+
+@pytest.mark.parametrize("N", [32768, 32769])
+def test_warp_unit_and_cta_kernels_at_the_switch(O, N):
+    """Plain passes with N ≤ 32768 run one unit per warp, larger N one unit per CTA: both
+    kernels against the oracle at the switch, through solve_slice (ragged M vs 8 units/CTA)."""
+    s, P = pair(O, n=3, delta=0.01, T=1.0, K=2, Kp=2, N=N, seed=I.C2.seed, system="dubins_rel",
+                target="disk", tgt_params=(5.0,))
+    x = I.random_queries(3, 13, -9, 9, seed=N)
+    _compare_solve(O, s, P, x, qid_base=77)
