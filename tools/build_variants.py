@@ -19,6 +19,7 @@ VARIANTS = {
     "gu2": ["-DHJMC_GROUP_UNROLL=2"],
     "wu0": ["-DHJMC_WARP_UNIT_MAX_N=0"],
     "wu64k": ["-DHJMC_WARP_UNIT_MAX_N=65536"],
+    "wuall": ["-DHJMC_WARP_UNIT_MAX_N=4294967295u"],
 }
 
 if __name__ == "__main__":

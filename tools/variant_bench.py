@@ -15,8 +15,9 @@ _lib.load("{lib}")
 from paper_2605_18566_b200.solver import Solver, SolverConfig
 p = I.BY_INDEX[{cfg}]
 kw = {kw}
+skw = {{k: kw.pop(k) for k in ("skip_stationary", "reuse_passes") if k in kw}}
 p = p.with_(**kw) if kw else p
-s = Solver(SolverConfig.from_preset(p))
+s = Solver(SolverConfig.from_preset(p, **skw))
 x = torch.from_numpy(I.queries(p)).cuda()
 out = s.alloc_result(x.shape[0])
 for _ in range(2): s.solve_slice(x, out=out)
