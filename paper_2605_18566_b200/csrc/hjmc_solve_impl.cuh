@@ -665,6 +665,20 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
 #define HJMC_WARP_UNIT_MAX_N 32768
 #endif
 constexpr uint32_t kWarpUnitMaxN = HJMC_WARP_UNIT_MAX_N;
+// ...and only when the units alone give every SM at least this many warps (a unit per warp
+// leaves a small grid's SMs under-occupied; a 40×40 slice is better served one unit per CTA).
+#ifndef HJMC_WARP_UNIT_MIN_WARPS_PER_SM
+#define HJMC_WARP_UNIT_MIN_WARPS_PER_SM 16
+#endif
+constexpr int kWarpUnitMinWarpsPerSm = HJMC_WARP_UNIT_MIN_WARPS_PER_SM;
+
+inline int sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 148;
+  return n;
+}
 
 template <class Tgt, int NDIM, int NT>
 cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
@@ -678,7 +692,7 @@ cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
   }
   if (p.proposal) {
     solve_kernel<Tgt, NDIM, NT, false, true><<<(unsigned)units, NT, 0, s>>>(p);
-  } else if (p.N <= kWarpUnitMaxN) {
+  } else if (p.N <= kWarpUnitMaxN && units >= (int64_t)kWarpUnitMinWarpsPerSm * sm_count()) {
     constexpr int kPerCta = NT / 32;
     const int64_t ctas = (units + kPerCta - 1) / kPerCta;
     solve_kernel<Tgt, NDIM, NT, false, false, 32><<<(unsigned)ctas, NT, 0, s>>>(p);

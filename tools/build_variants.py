@@ -20,6 +20,8 @@ VARIANTS = {
     "wu0": ["-DHJMC_WARP_UNIT_MAX_N=0"],
     "wu64k": ["-DHJMC_WARP_UNIT_MAX_N=65536"],
     "wuall": ["-DHJMC_WARP_UNIT_MAX_N=4294967295u"],
+    "wumin0": ["-DHJMC_WARP_UNIT_MIN_WARPS_PER_SM=0"],
+    "wumin16": ["-DHJMC_WARP_UNIT_MIN_WARPS_PER_SM=16"],
 }
 
 if __name__ == "__main__":

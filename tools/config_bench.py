@@ -20,9 +20,9 @@ SUBSET = {1: None, 2: None, 3: 4096, 4: 2048, 5: 1184}
 
 
 def run(idx, full_slice=False):
-    p = I.BY_INDEX[idx]
+    p = I.BY_INDEX[idx] if isinstance(idx, int) else I.PRESETS[idx]
     x_all = I.queries(p)
-    sub = SUBSET[idx]
+    sub = SUBSET.get(idx)
     if full_slice:      # one complete 2-D slice (the first), measured rather than extrapolated
         sub = None
         x_all = x_all[: p.grid_pts * p.grid_pts]
@@ -66,6 +66,8 @@ def run(idx, full_slice=False):
 
 
 if __name__ == "__main__":
-    which = [int(a.lstrip("c")) for a in sys.argv[1:] if a.startswith("c")] or [2, 3, 4, 5]
+    which = [int(a.lstrip("c")) if a[1:].isdigit() else a
+             for a in sys.argv[1:] if (a.startswith("c") and a[1:].isdigit()) or a in I.PRESETS]
+    which = which or [2, 3, 4, 5]
     for i in which:
         run(i, full_slice="--full-slice" in sys.argv)

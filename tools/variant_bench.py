@@ -13,7 +13,7 @@ sys.path.insert(0, "{root}")
 from paper_2605_18566_b200 import _lib, inputs as I
 _lib.load("{lib}")
 from paper_2605_18566_b200.solver import Solver, SolverConfig
-p = I.BY_INDEX[{cfg}]
+p = I.BY_INDEX[{cfg}] if isinstance({cfg}, int) else I.PRESETS[{cfg}]
 kw = {kw}
 skw = {{k: kw.pop(k) for k in ("skip_stationary", "reuse_passes") if k in kw}}
 p = p.with_(**kw) if kw else p
@@ -31,7 +31,8 @@ print(json.dumps({{"ms": ms, "evals_per_s": p.M * p.N * p.K * p.Kp / (ms / 1e3)}
 '''
 
 if __name__ == "__main__":
-    cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "2"
+    cfg = int(cfg) if cfg.isdigit() else repr(cfg)
     kw = json.loads(sys.argv[2]) if len(sys.argv) > 2 else {}
     reps = 3
     for lib in sorted(glob.glob(os.path.join(ROOT, "variants", "libhjmc_*.so"))):
