@@ -564,9 +564,26 @@ def test_binding_validates_shapes():
 
 @pytest.mark.parametrize("N", [32768, 32769])
 def test_warp_unit_and_cta_kernels_at_the_switch(O, N):
-    """Plain passes with N ≤ 32768 run one unit per warp, larger N one unit per CTA: both
-    kernels against the oracle at the switch, through solve_slice (ragged M vs 8 units/CTA)."""
-    s, P = pair(O, n=3, delta=0.01, T=1.0, K=2, Kp=2, N=N, seed=I.C2.seed, system="dubins_rel",
-                target="disk", tgt_params=(5.0,))
-    x = I.random_queries(3, 13, -9, 9, seed=N)
-    _compare_solve(O, s, P, x, qid_base=77)
+    """Plain passes with N ≤ 32768 and ≥ 16 units per SM run one unit per warp, others one
+    unit per CTA: both kernels against the oracle at the N switch (2,400 ragged units)."""
+    s, P = pair(O, n=3, delta=0.01, N=N, seed=I.C2.seed, system="dubins_rel", target="disk",
+                tgt_params=(5.0,))
+    M = 2400
+    x = I.random_queries(3, M, -9, 9, seed=N)
+    cc = np.full(M, 4.0, dtype=np.float32)
+    v, dv = s.value_grad(x, cc, 0.8, j_tag=3, k_tag=1, qid_base=77)
+    ids = np.arange(0, M, 7)                       # the oracle on every 7th query
+    ref = [O.phi(P, x[i].astype(np.float64), 4.0, 0.8, qid=77 + int(i), jw=3, kw=1) for i in ids]
+    vo = np.array([r[0] for r in ref])
+    dvo = np.array([r[1] for r in ref])
+    assert_v(v.cpu().numpy()[ids], vo)
+    assert_dv(dv.cpu().numpy()[ids], dvo)
+
+
+def test_warp_unit_solve_slice_ragged(O):
+    """The warp-per-unit kernel through solve_slice with a unit count that is not a multiple of
+    8 units per CTA (M·K = 2,403 ≥ 16 warps × 148 SMs)."""
+    s, P = pair(O, n=3, delta=0.01, T=1.0, K=3, Kp=2, N=700, seed=I.C2.seed,
+                system="dubins_rel", target="disk", tgt_params=(5.0,))
+    x = I.random_queries(3, 801, -9, 9, seed=5)
+    _compare_solve(O, s, P, x, qid_base=11)
