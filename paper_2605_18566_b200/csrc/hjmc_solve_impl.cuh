@@ -220,10 +220,14 @@ __device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, flo
 // the group min, every lane forms the same weight, lane ℓ = 0's S is the one reduced. A lane
 // keeps 12 + 12 + 12 live floats instead of 45 + 45 + 45, so 4 CTAs fit per SM (255 → ≤ 64
 // registers). Same samples, same counters, same arithmetic as the generic path.
+// Targets whose core is a min over (x, y) pairs of 3-coordinate blocks: the K-pair union and the
+// paper's pursuit-min, where every lane also needs the evader's sampled position — it
+// lives in one lane and reaches the others by two shuffles.
 template <class Tgt, int NDIM>
 struct UseLaneGroups {
-  static constexpr bool value = std::is_same<Tgt, PairUnion<NDIM>>::value && NDIM >= 37 &&
-                                NDIM <= 48;
+  static constexpr bool kPursuit = std::is_same<Tgt, PursuitMin<NDIM>>::value;
+  static constexpr bool value =
+      (std::is_same<Tgt, PairUnion<NDIM>>::value || kPursuit) && NDIM >= 37 && NDIM <= 48;
 };
 
 #ifndef HJMC_LG_LANES
@@ -235,7 +239,7 @@ constexpr int kLgLanes = HJMC_LG_LANES;
 constexpr int kLgSpan = 48 / kLgLanes;
 static_assert(kLgLanes == 2 || kLgLanes == 4, "lane groups of 2 or 4");
 
-template <int NDIM, int NT, bool kMaxMode>
+template <int NDIM, int NT, bool kMaxMode, bool kPursuit = false>
 __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float tau, float sigma_s,
                                         float A, float B, uint32_t w1base, uint32_t qid,
                                         float& S, float (&Mb)[kLgSpan], float& amax) {
@@ -270,12 +274,27 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
       box_muller_hat<true>(w.z, w.w, z[4 * qd + 2], z[4 * qd + 3]);
     }
     float best = 3.0e38f;
+    if constexpr (kPursuit) {
+      // the evader (last agent, coordinates kE, kE + 1) is owned by lane kE / kLgSpan
+      constexpr int kE = NDIM - 3, kLaneE = kE / kLgSpan, kCE = kE % kLgSpan;
+      const int src = (lane & ~(kLgLanes - 1)) | kLaneE;
+      const float ex = __shfl_sync(0xffffffffu, fmaf(sigma_s, z[kCE], xb[kCE]), src);
+      const float ey = __shfl_sync(0xffffffffu, fmaf(sigma_s, z[kCE + 1], xb[kCE + 1]), src);
 #pragma unroll
-    for (int pq = 0; pq < kTriples; ++pq) {
-      const float a = fmaf(sigma_s, z[3 * pq], xb[3 * pq]);
-      const float b = fmaf(sigma_s, z[3 * pq + 1], xb[3 * pq + 1]);
-      const float r2 = fmaf(a, a, b * b);
-      best = (kLgSpan * l + 3 * pq + 1 < NDIM) ? fminf(best, r2) : best;
+      for (int pq = 0; pq < kTriples; ++pq) {
+        const float a = fmaf(sigma_s, z[3 * pq], xb[3 * pq]) - ex;
+        const float b = fmaf(sigma_s, z[3 * pq + 1], xb[3 * pq + 1]) - ey;
+        const float r2 = fmaf(a, a, b * b);
+        best = (kLgSpan * l + 3 * pq < kE) ? fminf(best, r2) : best;   // pursuers only
+      }
+    } else {
+#pragma unroll
+      for (int pq = 0; pq < kTriples; ++pq) {
+        const float a = fmaf(sigma_s, z[3 * pq], xb[3 * pq]);
+        const float b = fmaf(sigma_s, z[3 * pq + 1], xb[3 * pq + 1]);
+        const float r2 = fmaf(a, a, b * b);
+        best = (kLgSpan * l + 3 * pq + 1 < NDIM) ? fminf(best, r2) : best;
+      }
     }
 #pragma unroll
     for (int o = 1; o < kLgLanes; o <<= 1) best = fminf(best, __shfl_xor_sync(0xffffffffu, best, o));
@@ -585,7 +604,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
     if (hit < 0) {
       if constexpr (kLG) {
         float S, Mb[kLgSpan], amax;
-        lg_pass<NDIM, NT, false>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax);
+        lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax);
         lg_reduce<NDIM, NT>(sm, S, Mb);
       } else {
         float S, Mz[NDIM];
@@ -599,7 +618,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         float amax_t;
         if constexpr (kLG) {
           float S, Mb[kLgSpan];
-          lg_pass<NDIM, NT, true>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax_t);
+          lg_pass<NDIM, NT, true, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax_t);
         } else {
           amax_t = mc_max_exponent<Tgt, NDIM, GS>(tgt, ctr, sigma_s, A, P.N, P.antithetic, w1base,
                                                   id, P.tag, P.rk, tz, tid);
@@ -616,7 +635,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         B = -sm.shift;
         if constexpr (kLG) {
           float S, Mb[kLgSpan], am;
-          lg_pass<NDIM, NT, false>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, am);
+          lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, am);
           lg_reduce<NDIM, NT>(sm, S, Mb);
         } else {
           float S, Mz[NDIM];
