@@ -70,6 +70,7 @@ def test_c1_value_grad_full_grid(O, visc):
     ("rel_disk6", 6, (1.5,), "rocket6", 12.0, 1.0, -6, 6),
     ("pair_union", 15, (1.0,), "dubins_pairs", 20.0, 1.0, -4, 4),
     ("pair_union", 45, (1.0,), "dubins_pairs", 0.05, 0.3, -4, 4),
+    ("pursuit_min", 45, (1.5,), "multiagent", 5.0, 0.4, -6, 6),      # lane groups + evader shuffle
     ("quad_bowl", 45, (0.25,), "quadratic", 5.0, 0.2, -0.5, 0.5),
     ("quad_bowl", 1, (0.25,), "quadratic", 5.0, 0.2, -2, 2),
     ("linear", 3, (0.5, -1.0, 2.0, 0.3), "quadratic", 4.0, 0.5, -2, 2),
