@@ -31,7 +31,10 @@ def run(idx, full_slice=False):
     x = torch.from_numpy(x_all[ids]).cuda()
     qid = torch.from_numpy(ids.astype(np.int32)).cuda()
     out = s.alloc_result(len(ids), hist=False)
-    s.solve_slice(x[: min(len(ids), 296)], qid=qid[: min(len(ids), 296)])   # warm
+    # warm up with the launch actually timed (the kernel variant depends on M·K and N: lazy
+    # module loading would otherwise land in the timed region) unless that launch is long
+    warm = len(ids) if len(ids) * p.N * p.K * p.Kp < 2e11 else min(len(ids), 296)
+    s.solve_slice(x[:warm], qid=qid[:warm])
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -45,7 +48,7 @@ def run(idx, full_slice=False):
     # the same subset with the exact shortcuts (bit-identical outputs): stationary skip + memo
     f = Solver(SolverConfig.from_preset(p, skip_stationary=True, reuse_passes=True))
     fout = f.alloc_result(len(ids), hist=False)
-    f.solve_slice(x[: min(len(ids), 296)], qid=qid[: min(len(ids), 296)])
+    f.solve_slice(x[:warm], qid=qid[:warm])
     torch.cuda.synchronize()
     f.pass_count()
     e0.record()
