@@ -67,14 +67,15 @@ def dist_env():
 # ---- clocks sampled during the timed region ----------------------------------------------------
 class ClockSampler:
     """SM clock, power and throttle reasons sampled by NVML in a background thread (every
-    200 ms) while the timed region runs — in-process, so no polling subprocess competes."""
+    100 ms: ≥ 10 Hz) while the timed region runs — in-process, so no polling
+    subprocess competes."""
 
     REASONS = {  # NVML clocks-event-reason bits
         "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
         "sw_power_cap": 0x4,
     }
 
-    def __init__(self, index: int, period_s: float = 0.2):
+    def __init__(self, index: int, period_s: float = 0.1):
         self.index, self.period = index, period_s
         self.rows, self.stop_evt, self.thread, self.h = [], threading.Event(), None, None
 
@@ -116,7 +117,7 @@ class ClockSampler:
         reasons = sorted({k for r in self.rows for k, bit in self.REASONS.items() if r[2] & bit})
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(smax), "sm_min_mhz": min(sm),
                 "samples": len(self.rows), "reasons": reasons,
-                "power_w_max": max(r[1] for r in self.rows), "source": "NVML, 200 ms"}
+                "power_w_max": max(r[1] for r in self.rows), "source": "NVML, 100 ms"}
 
 
 # ---- CPU oracle (cpu_baseline leg and the reference arm) --------------------------------------
