@@ -332,7 +332,8 @@ def run_ours(args):
             "pipe": pipe, "ops_per_eval": rl["ops"],
             "peak_basis": f"{rl['rate']:.0f} lane-ops/clk/SM × 148 SMs × 1965 MHz (sm_max); "
                           f"rates: {rate_src}",
-            "kernel": "solve_kernel<Disk<3>,3,256> (+ tube epilogue, <0.1%)",
+            "kernel": f"solve_kernel<{preset.target}, n={preset.n}, 256 threads> "
+                      "(+ tube epilogue, <0.1%)",
             "kernel_ms_avg": kern_avg_ms}
     if clk and clk.get("sm_mhz"):
         roof["frac_at_measured_clock"] = roof["frac"] * 1965.0 / clk["sm_mhz"]
@@ -389,7 +390,7 @@ def run_ours(args):
                    "K": preset.K, "Kp": preset.Kp, "system": preset.system,
                    "target": preset.target, "delta": preset.delta, "T": preset.T,
                    "parallelism": f"query-sharded x{world} (one slice per GPU, no collective)",
-                   "l2": "flushed between steps (256 MB write); inputs 122 KB"},
+                   "l2": f"flushed between steps (256 MB write); inputs {x_host.nbytes // 1024} KB"},
         "s_per_slice": (total_ms / 1000.0 / args.steps) * world / slices,
         "kernel_ms_per_step": kern_avg_ms,
         "gpu_launches": 2 * args.steps,
