@@ -303,6 +303,25 @@ HJMC_API int hjmc_picard_begin(hjmc_handle* h, const float* x, const uint32_t* q
 HJMC_API int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, float* v,
                               float* dv, float* c, double* partials, void* stream);
 
+/* Algorithm 1 with its stopping test (iterate until ε_j(k) < tol, step 5), for every
+ * horizon, entirely on the device: hjmc_picard_begin, then one CUDA graph whose conditional
+ * 'while' node repeats {Φ pass of the still-active horizons, residual partials, decision} —
+ * the decision kernel computes ε_j(k) = sqrt(Σ(v^(k+1)−v^(k))² / Σ(v^(k))²) over this handle's
+ * queries (R11; single process — sharded slices use hjmc_picard_pass and an all-reduce),
+ * retires horizon j when ε_j(k) < tol, and stops the loop when none is left or after max_iter
+ * passes. Outputs (device): v [K][M], dv [K][M][n] (may be NULL), c [K][M] (may be NULL) of each
+ * horizon's final iterate; iters [K] (int32) passes run per horizon; eps, dsup [K][max_iter]
+ * (double) ε_j(k) and max_m |v^(k+1) − v^(k)|, NaN past the stop. Same kernels, counters and
+ * reduction order as hjmc_picard_pass driven from the host: identical results. Stream-ordered
+ * (asynchronous): one graph launch on stream; the instantiated graph is cached in the handle and
+ * reused while the arguments and the handle's dynamics / target / avoid set are unchanged.
+ * x, qid, drift and the outputs must stay valid until the stream reaches the launch.
+ * EINVAL for M < 1, max_iter < 1, tol < 0 or missing outputs. */
+HJMC_API int hjmc_picard_solve(hjmc_handle* h, const float* x, const uint32_t* qid,
+                               uint32_t qid_base, int64_t M, const float* drift, double tol,
+                               int32_t max_iter, float* v, float* dv, float* c, int32_t* iters,
+                               double* eps, double* dsup, void* stream);
+
 /* g(x) and the analytic Dg(x) used for c^(0) (dev pointers; dg may be NULL). */
 HJMC_API int hjmc_eval_target(hjmc_handle* h, const float* x, int64_t M, float* g, float* dg,
                      void* stream);

@@ -29,7 +29,8 @@ EXPORTS = [
     "hjmc_supported", "hjmc_value_grad", "hjmc_solve_slice", "hjmc_solve_slice_host",
     "hjmc_eval_target", "hjmc_eval_hamiltonian", "hjmc_debug_normals", "hjmc_check",
     "hjmc_last_bad_query", "hjmc_last_error", "hjmc_residual_partials", "hjmc_version",
-    "hjmc_pass_count", "hjmc_picard_begin", "hjmc_picard_pass", "hjmc_set_avoid",
+    "hjmc_pass_count", "hjmc_picard_begin", "hjmc_picard_pass", "hjmc_picard_solve",
+    "hjmc_set_avoid",
 ]
 
 
@@ -92,6 +93,8 @@ def load(path: str = LIB_PATH):
     L.hjmc_set_avoid.argtypes = [vp, C.c_int32, C.POINTER(C.c_float), C.c_int32]
     L.hjmc_picard_begin.argtypes = [vp, vp, vp, u32, i64, vp, vp]
     L.hjmc_picard_pass.argtypes = [vp, C.c_int32, vp, vp, vp, vp, vp, vp]
+    L.hjmc_picard_solve.argtypes = [vp, vp, vp, u32, i64, vp, C.c_double, C.c_int32, vp, vp, vp,
+                                    vp, vp, vp, vp]
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"libhjmc.so lacks {name}")

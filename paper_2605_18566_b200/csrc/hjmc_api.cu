@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -52,6 +53,13 @@ struct hjmc_handle {
   size_t partial_cap = 0;
   int64_t last_bad = -1;
   std::string err;
+  // device-resident Algorithm 1 (hjmc_picard_solve): the instantiated graph, reused while the
+  // call's arguments and the handle's problem (generation) are unchanged
+  unsigned generation = 0;
+  int* d_pstate = nullptr;          // [K] horizons 1..K, [K] activity mask, [1] iterate counter
+  cudaGraph_t pic_graph = nullptr;
+  cudaGraphExec_t pic_exec = nullptr;
+  std::vector<uintptr_t> pic_key;
 };
 
 namespace {
@@ -212,6 +220,9 @@ void hjmc_destroy(hjmc_handle* h) {
   if (h->d_vtmp) cudaFree(h->d_vtmp);
   if (h->d_active) cudaFree(h->d_active);
   if (h->d_partial) cudaFree(h->d_partial);
+  if (h->pic_exec) cudaGraphExecDestroy(h->pic_exec);
+  if (h->pic_graph) cudaGraphDestroy(h->pic_graph);
+  if (h->d_pstate) cudaFree(h->d_pstate);
   if (h->host_stream) cudaStreamDestroy(h->host_stream);
   delete h;
 }
@@ -260,6 +271,7 @@ int hjmc_set_dynamics(hjmc_handle* h, int32_t id, const float* params, int32_t n
   }
   h->sp = sp;
   h->sys_set = true;
+  ++h->generation;
   return HJMC_OK;
 }
 
@@ -280,6 +292,7 @@ int hjmc_set_avoid(hjmc_handle* h, int32_t id, const float* params, int32_t np) 
   }
   a.type = id;
   h->avoid = a;
+  ++h->generation;
   return HJMC_OK;
 }
 
@@ -327,6 +340,7 @@ int hjmc_set_target(hjmc_handle* h, int32_t id, const float* params, int32_t np)
   h->tgt_id = id;
   h->ks = ks;
   h->tgt_set = true;
+  ++h->generation;
   return HJMC_OK;
 }
 
@@ -499,6 +513,172 @@ int hjmc_picard_begin(hjmc_handle* h, const float* x, const uint32_t* qid, uint3
   ip.tp = h->tp;
   cudaError_t e = h->ks.picard_init(ip, (cudaStream_t)stream);
   return e == cudaSuccess ? HJMC_OK : cuda_fail(h, e, "picard init launch");
+}
+
+// Device-resident Algorithm 1: the same init / pass / residual kernels as hjmc_picard_begin and
+// hjmc_picard_pass, ordered in one CUDA graph — init, then a conditional 'while' node looping
+// {pass, residual, decision} whose condition the decision kernel sets — so no Picard iterate
+// returns to the host. Results are bit-identical to the host-driven loop (same kernels, same
+// reduction orders, the same double-precision test). The instantiated graph is cached in the
+// handle and relaunched while the arguments and the problem are unchanged.
+int hjmc_picard_solve(hjmc_handle* h, const float* x, const uint32_t* qid, uint32_t qid_base,
+                      int64_t M, const float* drift, double tol, int32_t max_iter, float* v,
+                      float* dv, float* c, int32_t* iters, double* eps, double* dsup,
+                      void* stream) {
+  int rc = ready(h);
+  if (rc) return rc;
+  if (M < 1 || !x) return fail(h, HJMC_EINVAL, "need M >= 1 and x");
+  if (M * (int64_t)h->cfg.K > 0x7FFFFFFFLL) return fail(h, HJMC_EINVAL, "M*K exceeds 2^31-1");
+  if (max_iter < 1 || !(tol >= 0.0)) return fail(h, HJMC_EINVAL, "need max_iter >= 1, tol >= 0");
+  if (!v || !iters || !eps || !dsup) return fail(h, HJMC_EINVAL, "v, iters, eps, dsup required");
+  if (!h->cfg.crn && max_iter > 256) return fail(h, HJMC_EINVAL, "max_iter must be <= 256 without crn");
+  if ((rc = set_device(h))) return rc;
+  const int K = h->cfg.K;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t KM = (size_t)M * (size_t)K;
+  const int blocks = (int)std::min<int64_t>(148, (M + 255) / 256);
+  const size_t need = (size_t)K * (size_t)blocks * 3;
+  // handle scratch (sizes only grow; a reallocation invalidates the cached graph)
+  bool realloc = false;
+  if (KM > h->cstate_cap) {
+    if (h->d_cstate) cudaFree(h->d_cstate);
+    h->d_cstate = nullptr;
+    h->cstate_cap = 0;
+    if (cudaMalloc((void**)&h->d_cstate, KM * sizeof(double)) != cudaSuccess)
+      return fail(h, HJMC_ENOMEM, "picard state allocation failed");
+    h->cstate_cap = KM;
+    realloc = true;
+  }
+  const float* old_vprev = h->d_vprev;
+  if ((rc = ensure(h, &h->d_vprev, &h->vprev_cap, KM))) return rc;
+  realloc = realloc || h->d_vprev != old_vprev;
+  if (need > h->partial_cap) {
+    if (h->d_partial) cudaFree(h->d_partial);
+    h->d_partial = nullptr;
+    h->partial_cap = 0;
+    if (cudaMalloc((void**)&h->d_partial, need * sizeof(double)) != cudaSuccess)
+      return fail(h, HJMC_ENOMEM, "picard partials allocation failed");
+    h->partial_cap = need;
+    realloc = true;
+  }
+  if (!h->d_pstate) {
+    if (cudaMalloc((void**)&h->d_pstate, (2 * 65536 + 1) * sizeof(int)) != cudaSuccess)
+      return fail(h, HJMC_ENOMEM, "picard state allocation failed");
+    realloc = true;
+  }
+  h->pic_x = x;
+  h->pic_qid = qid;
+  h->pic_qid_base = qid_base;
+  h->pic_M = M;
+  h->pic_drift = drift;
+  double tol_bits = tol;
+  uintptr_t tol_key;
+  std::memcpy(&tol_key, &tol_bits, sizeof(tol_key));
+  const std::vector<uintptr_t> key = {
+      (uintptr_t)x, (uintptr_t)qid, qid_base, (uintptr_t)M, (uintptr_t)drift, tol_key,
+      (uintptr_t)max_iter, (uintptr_t)v, (uintptr_t)dv, (uintptr_t)c, (uintptr_t)iters,
+      (uintptr_t)eps, (uintptr_t)dsup, h->generation};
+  cudaError_t e;
+  if (realloc || !h->pic_exec || key != h->pic_key) {
+    if (h->pic_exec) cudaGraphExecDestroy(h->pic_exec);
+    if (h->pic_graph) cudaGraphDestroy(h->pic_graph);
+    h->pic_exec = nullptr;
+    h->pic_graph = nullptr;
+    h->pic_key.clear();
+    int* st = h->d_pstate;
+    PicardInitParams ip{};
+    ip.x = x;
+    ip.M = M;
+    ip.K = K;
+    ip.c_state = h->d_cstate;
+    ip.v_prev = h->d_vprev;
+    ip.gp.delta_eff = delta_eff(h->cfg);
+    ip.gp.m0 = h->cfg.m0;
+    ip.gp.c_min = h->cfg.c_min;
+    ip.gp.c_max = h->cfg.c_max;
+    ip.sp = h->sp;
+    ip.tp = h->tp;
+    SolveParams p;
+    fill_common(h, &p);
+    p.x = x;
+    p.drift = drift;
+    p.qid = qid;
+    p.qid_base = qid_base;
+    p.M = M;
+    p.K = K;
+    p.Kp = 1;
+    p.T = (double)h->cfg.T;
+    p.mode = kModePass;
+    p.v = v;
+    p.dv = dv;
+    p.c_out = c;
+    p.c_state = h->d_cstate;
+    p.active_j = st;
+    p.n_active = K;
+    p.active_mask = st + K;
+    p.kiter_dev = st + 2 * K;
+    p.kiter = 0;
+    p.skip_stationary = 0;
+    p.reuse_passes = 0;
+
+    cudaGraph_t graph = nullptr;
+    cudaGraphConditionalHandle cond;
+    auto bail = [&](cudaError_t err, const char* where) {
+      if (graph) cudaGraphDestroy(graph);
+      return cuda_fail(h, err, where);
+    };
+    if ((e = cudaGraphCreate(&graph, 0)) != cudaSuccess) return bail(e, "graph create");
+    if ((e = cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault)) !=
+        cudaSuccess)
+      return bail(e, "conditional handle");
+    cudaStream_t cap = h->host_stream;
+    // 1. init: v^(0) = g, c^(0) = Γ(x, Dg) per horizon; loop state, iteration counts, NaN histories
+    if ((e = cudaStreamBeginCaptureToGraph(cap, graph, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+      return bail(e, "init capture");
+    cudaError_t le = h->ks.picard_init(ip, cap);
+    if (le == cudaSuccess) le = launch_picard_solve_init(st, K, iters, eps, dsup, max_iter, cap);
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaStreamCaptureStatus cs;
+    std::vector<cudaGraphNode_t> tail;
+    if (le == cudaSuccess &&
+        (le = cudaStreamGetCaptureInfo(cap, &cs, nullptr, nullptr, &deps, &ndeps)) == cudaSuccess)
+      tail.assign(deps, deps + ndeps);
+    cudaGraph_t captured = nullptr;
+    e = cudaStreamEndCapture(cap, &captured);
+    if (le != cudaSuccess) return bail(le, "init launches");
+    if (e != cudaSuccess) return bail(e, "init capture end");
+    // 2. the loop
+    cudaGraphNode_t node;
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    if ((e = cudaGraphAddNode(&node, graph, tail.data(), tail.size(), &np)) != cudaSuccess)
+      return bail(e, "conditional node");
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    if ((e = cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+      return bail(e, "body capture");
+    le = h->ks.solve(p, M * (int64_t)K, cap);
+    if (le == cudaSuccess)
+      le = launch_picard_residual(v, h->d_vprev, M, st, K, h->d_partial, blocks, cap);
+    if (le == cudaSuccess)
+      le = launch_picard_decide(h->d_partial, K, blocks, tol, max_iter, st + K, st + 2 * K, iters,
+                                eps, dsup, cond, cap);
+    e = cudaStreamEndCapture(cap, &captured);
+    if (le != cudaSuccess) return bail(le, "body launches");
+    if (e != cudaSuccess) return bail(e, "body capture end");
+    cudaGraphExec_t exec = nullptr;
+    if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) return bail(e, "graph instantiate");
+    h->pic_graph = graph;
+    h->pic_exec = exec;
+    h->pic_key = key;
+  }
+  if ((e = cudaGraphLaunch(h->pic_exec, s)) != cudaSuccess) return cuda_fail(h, e, "graph launch");
+  return sync_check_if_requested(h, s);
 }
 
 int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, float* v, float* dv,

@@ -1,6 +1,8 @@
 // hjmc_aux.cu — small non-templated kernels: tube epilogue, H/Γ evaluator, RNG debug dump.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cstdint>
 
 #include "hjmc_kernels.cuh"
@@ -107,7 +109,63 @@ __global__ void picard_residual_kernel(const float* __restrict__ v, float* __res
   }
 }
 
+__global__ void picard_decide_kernel(const double* __restrict__ partial, int K, int blocks,
+                                     double tol, int max_iter, int* mask, int* kiter, int* iters,
+                                     double* eps, double* dsup, cudaGraphConditionalHandle cond) {
+  if (threadIdx.x != 0) return;  // K is small; one thread keeps the host driver's order
+  const int k = *kiter;
+  int any = 0;
+  for (int j = 0; j < K; ++j) {
+    if (!mask[j]) continue;
+    double num = 0.0, den = 0.0, mx = 0.0;
+    for (int b = 0; b < blocks; ++b) {
+      const double* q = partial + ((size_t)j * blocks + b) * 3;
+      num += q[0];
+      den += q[1];
+      mx = fmax(mx, q[2]);
+    }
+    const double e = sqrt(num / fmax(den, 1e-300));
+    eps[(size_t)j * max_iter + k] = e;
+    dsup[(size_t)j * max_iter + k] = mx;
+    iters[j] = k + 1;
+    if (e < tol) mask[j] = 0;
+    else any = 1;
+  }
+  *kiter = k + 1;
+  cudaGraphSetConditional(cond, (any && k + 1 < max_iter) ? 1u : 0u);
+}
+
+__global__ void picard_solve_init_kernel(int* state, int K, int32_t* iters, double* eps,
+                                         double* dsup, int max_iter) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < K) {
+    state[i] = i + 1;
+    state[K + i] = 1;
+    iters[i] = 0;
+  }
+  if (i == 0) state[2 * K] = 0;
+  for (int t = i; t < K * max_iter; t += gridDim.x * blockDim.x) {
+    eps[t] = __longlong_as_double(0x7FF8000000000000LL);   // quiet NaN past each stop
+    dsup[t] = __longlong_as_double(0x7FF8000000000000LL);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_picard_solve_init(int* state, int K, int32_t* iters, double* eps,
+                                     double* dsup, int max_iter, cudaStream_t s) {
+  const int n = std::max(K, K * max_iter);
+  picard_solve_init_kernel<<<(n + 255) / 256, 256, 0, s>>>(state, K, iters, eps, dsup, max_iter);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_picard_decide(const double* partial, int K, int blocks, double tol,
+                                 int max_iter, int* mask, int* kiter, int* iters, double* eps,
+                                 double* dsup, cudaGraphConditionalHandle cond, cudaStream_t s) {
+  picard_decide_kernel<<<1, 32, 0, s>>>(partial, K, blocks, tol, max_iter, mask, kiter, iters, eps,
+                                        dsup, cond);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_picard_residual(const float* v, float* v_prev, int64_t M, const int* active_j,
                                    int n_active, double* partial, int blocks, cudaStream_t s) {

@@ -48,6 +48,10 @@ struct SolveParams {
   const int* active_j;             // [n_active] 1-based horizon indices (device)
   int n_active;
   int kiter;                       // Picard iterate index (counter word when crn = 0)
+  // device-resident Algorithm 1 (hjmc_picard_solve): per-horizon activity mask [K] and the
+  // iterate index read on the device (graph launches cannot change kernel arguments)
+  const int* active_mask;
+  const int* kiter_dev;
 };
 
 enum : int { kModeSolve = 0, kModeValueGrad = 1, kModePass = 2 };
@@ -104,6 +108,16 @@ cudaError_t launch_hamiltonian(const EvalParams& p, cudaStream_t s);
 // max |v−v_prev|) over that block's queries; then v_prev ← v. Deterministic (fixed order).
 cudaError_t launch_picard_residual(const float* v, float* v_prev, int64_t M, const int* active_j,
                                    int n_active, double* partial, int blocks, cudaStream_t s);
+// Algorithm 1's stopping test on the device (hjmc_picard_solve): per active horizon j sum the
+// residual partials in fixed block order, ε_j(k) = sqrt(num / max(den, 1e-300)) (R11),
+// record ε, the sup-norm difference and the iterate count, retire j when ε < tol, advance k,
+// and set the graph's while-condition to (any horizon active && k < max_iter).
+cudaError_t launch_picard_decide(const double* partial, int K, int blocks, double tol,
+                                 int max_iter, int* mask, int* kiter, int* iters, double* eps,
+                                 double* dsup, cudaGraphConditionalHandle cond, cudaStream_t s);
+// Loop state for hjmc_picard_solve: horizons 1..K, all active, k = 0, iters = 0, NaN histories.
+cudaError_t launch_picard_solve_init(int* state, int K, int32_t* iters, double* eps,
+                                     double* dsup, int max_iter, cudaStream_t s);
 cudaError_t launch_debug_normals(int n, uint32_t qid, uint32_t jw, uint32_t kw, uint32_t i0,
                                  uint32_t count, const RoundKeys& rk, uint32_t tag, int antithetic, float* z,
                                  uint32_t* raw, cudaStream_t s);

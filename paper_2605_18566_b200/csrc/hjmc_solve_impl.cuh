@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
   } else if (P.mode == kModePass) {
     m = unit / P.n_active;
     j = P.active_j[unit % P.n_active];
+    if (P.active_mask && !P.active_mask[j - 1]) return;  // retired horizon (whole group)
   } else {
     m = unit;
     j = 1;
@@ -547,7 +548,9 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
 
   for (int k = 0; k < P.Kp; ++k) {
     const uint32_t kw = (P.mode == kModeSolve)  ? (P.crn ? 0u : (uint32_t)k)
-                        : (P.mode == kModePass) ? (P.crn ? 0u : (uint32_t)P.kiter)
+                        : (P.mode == kModePass) ? (P.crn ? 0u
+                                                   : (uint32_t)(P.kiter_dev ? *P.kiter_dev
+                                                                            : P.kiter))
                                                 : P.ktag;
     const uint32_t w1base = (kw << 8) | (jw << 16);
     const float A = opaque((float)(-c * kLog2e));
@@ -711,7 +714,11 @@ cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
   }
   if (p.proposal) {
     solve_kernel<Tgt, NDIM, NT, false, true><<<(unsigned)units, NT, 0, s>>>(p);
-  } else if (p.N <= kWarpUnitMaxN && units >= (int64_t)kWarpUnitMinWarpsPerSm * sm_count()) {
+  } else if (p.N <= kWarpUnitMaxN &&
+             (p.mode == kModeValueGrad ? p.M : p.M * (int64_t)p.K) >=
+                 (int64_t)kWarpUnitMinWarpsPerSm * sm_count()) {
+    // decided on the slice's full unit count, so a stepwise pass over a subset of horizons runs
+    // the same kernel (same reduction order) as the fused solve
     constexpr int kPerCta = NT / 32;
     const int64_t ctas = (units + kPerCta - 1) / kPerCta;
     solve_kernel<Tgt, NDIM, NT, false, false, 32><<<(unsigned)ctas, NT, 0, s>>>(p);

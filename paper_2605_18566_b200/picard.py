@@ -129,3 +129,36 @@ def torch_allreduce(group=None):
         return out
 
     return f
+
+
+def solve_adaptive_device(solver, x, tol: float, max_iter: int, qid_base: int = 0, qid=None,
+                          drift=None, want_dv: bool = True):
+    """Algorithm 1 with its stopping test in ONE device-resident call (hjmc_picard_solve: a CUDA
+    graph whose conditional while-node loops pass → residual → decision with no host round
+    trip). Single process only (sharded slices need the all-reduce of solve_adaptive). Returns
+    the same dict as solve_adaptive without the log: v, dv, c [K][M](…) tensors, iters [K],
+    eps / d_sup [K][max_iter] (NaN past the stop), tube [M], converged [K]."""
+    t = solver.torch
+    cfg = solver.cfg
+    x = solver._as_query(x)
+    M, K, n = x.shape[0], cfg.K, cfg.n
+    q = solver._as_dev(qid, t.int32) if qid is not None else None
+    b = solver._as_dev(drift) if drift is not None else None
+    dev = solver.device
+    v = t.empty((K, M), device=dev)
+    dv = t.empty((K, M, n), device=dev) if want_dv else None
+    c = t.empty((K, M), device=dev)
+    iters = t.zeros(K, dtype=t.int32, device=dev)
+    eps = t.empty((K, max_iter), dtype=t.float64, device=dev)
+    dsup = t.empty((K, max_iter), dtype=t.float64, device=dev)
+    ptr = lambda a: C.c_void_p(a.data_ptr()) if a is not None else None
+    solver._check(solver.L.hjmc_picard_solve(
+        solver.h, ptr(x), ptr(q), qid_base, M, ptr(b), float(tol), int(max_iter), ptr(v), ptr(dv),
+        ptr(c), ptr(iters), ptr(eps), ptr(dsup), solver._stream()))
+    g, _ = solver.eval_target(x)
+    tube = t.minimum(g, v.min(dim=0).values)
+    eps_h = eps.cpu().numpy()
+    it = iters.cpu().numpy().astype(np.int64)
+    conv = np.array([it[j] > 0 and eps_h[j, it[j] - 1] < tol for j in range(K)])
+    return {"v": v, "dv": dv, "c": c, "iters": it, "eps": eps_h, "d_sup": dsup.cpu().numpy(),
+            "tube": tube, "converged": conv, "g0": g}

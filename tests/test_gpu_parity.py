@@ -588,3 +588,31 @@ def test_warp_unit_solve_slice_ragged(O):
                 system="dubins_rel", target="disk", tgt_params=(5.0,))
     x = I.random_queries(3, 801, -9, 9, seed=5)
     _compare_solve(O, s, P, x, qid_base=11)
+
+
+@pytest.mark.parametrize("crn", [True, False])
+def test_picard_device_resident_equals_host_driven(O, crn):
+    """hjmc_picard_solve (Algorithm 1 as one CUDA graph with a conditional while-node) gives
+    the host-driven loop's results bit for bit: iteration counts, ε and sup-norm histories,
+    every horizon's final v / Dv / c — with horizons retiring at different iterates."""
+    from paper_2605_18566_b200.picard import solve_adaptive, solve_adaptive_device
+
+    p = I.C2.with_(N=3000, K=3)
+    x = I.queries(p)[::29]
+    s = Solver(SolverConfig.from_preset(p, crn=crn))
+    r0 = solve_adaptive(s, x, tol=0.0, max_iter=6)
+    e = np.sort(r0["eps"][np.isfinite(r0["eps"]) & (r0["eps"] > 0)])
+    tol = float(np.median(e))                            # some horizons stop early, some not
+    a = solve_adaptive(s, x, tol=tol, max_iter=6)
+    b = solve_adaptive_device(s, x, tol=tol, max_iter=6)
+    assert list(a["iters"]) == list(b["iters"]) and len(set(a["iters"])) >= 1
+    np.testing.assert_array_equal(a["eps"], b["eps"])
+    np.testing.assert_array_equal(a["d_sup"], b["d_sup"])
+    for k in ("v", "dv", "c", "tube"):
+        assert torch.equal(a[k], b[k]), k
+    assert list(a["converged"]) == list(b["converged"])
+    # an exactly stationary problem stops after the second pass (quadratic H, CRN: c = 1/δ)
+    q = Solver(SolverConfig(n=2, delta=0.05, T=0.5, K=2, N=2048, system="quadratic",
+                            target="quad_bowl", tgt_params=(0.25,)))
+    rq = solve_adaptive_device(q, I.queries(I.C1)[::9], tol=1e-9, max_iter=10)
+    assert list(rq["iters"]) == [2, 2] and np.all(rq["eps"][:, 1] == 0.0)
