@@ -180,9 +180,18 @@ struct SolveSmem {
   float shift;
 };
 
+// Barrier over the GS threads that share a unit in a CTA of CTA threads: the CTA barrier, the
+// warp, or named barrier 1 + group index (bar.sync id, GS).
+template <int GS, int CTA>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (GS == CTA) __syncthreads();
+  else if constexpr (GS == 32) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / GS)), "r"(GS) : "memory");
+}
+
 // Group-wide merge of (S, Mz[NDIM]) into sm.sum (double), deterministic order. NT = group
-// size: the CTA (shared-memory merge across its warps) or one warp (shuffles only).
-template <int NDIM, int NT>
+// size: the CTA or a part of it (shared-memory merge across its warps) or one warp (shuffles).
+template <int NDIM, int NT, int CTA = NT>
 __device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, float (&Mz)[NDIM],
                                            uint32_t tid) {
   const int lane = tid & 31, warp = tid >> 5;
@@ -203,14 +212,14 @@ __device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, flo
 #pragma unroll
     for (int d = 0; d < NDIM; ++d) sm.part[warp][1 + d] = Mz[d];
   }
-  __syncthreads();
+  group_sync<NT, CTA>();
   for (int col = tid; col < NDIM + 1; col += NT) {
     double acc = 0.0;
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) acc += (double)sm.part[w][col];
     sm.sum[col] = acc;
   }
-  __syncthreads();
+  group_sync<NT, CTA>();
 }
 
 // ---- lane-group layout for the K-pair union at n = 39..48 (C5: n = 45) -----------------------
@@ -478,14 +487,12 @@ constexpr int min_blocks() {
 // unit overlap the sampling of the CTA's other seven, and no __syncthreads exists).
 template <class Tgt, int NDIM, int NT, bool kLG = false, bool kProp = false, int GS = NT>
 __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(const __grid_constant__ SolveParams P) {
-  static_assert(GS == NT || (GS == 32 && !kLG), "warp-per-unit only for the generic kernel");
+  static_assert(GS == NT || (!kLG && GS >= 32 && NT % GS == 0 && GS % 32 == 0),
+                "thread groups smaller than the CTA only for the generic kernel");
   __shared__ SolveSmem<NDIM, GS> smv[NT / GS];
   SolveSmem<NDIM, GS>& sm = smv[threadIdx.x / GS];
   const uint32_t tid = threadIdx.x % GS;
-  auto gsync = [] {
-    if constexpr (GS == NT) __syncthreads();
-    else __syncwarp();
-  };
+  auto gsync = [] { group_sync<GS, NT>(); };
   const int64_t unit = (int64_t)blockIdx.x * (NT / GS) + threadIdx.x / GS;
   if constexpr (GS != NT) {
     const int64_t units = (P.mode == kModeSolve)  ? P.M * (int64_t)P.K
@@ -613,7 +620,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         float S, Mz[NDIM];
         mc_accumulate<Tgt, NDIM, GS, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base, id,
                                             P.tag, P.rk, S, Mz, tz, tid);
-        cta_reduce<NDIM, GS>(sm, S, Mz, tid);
+        cta_reduce<NDIM, GS, NT>(sm, S, Mz, tid);
       }
       if (!(sm.sum[0] >= (double)kUnderflowS)) {
         // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with
@@ -644,7 +651,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
           float S, Mz[NDIM];
           mc_accumulate<Tgt, NDIM, GS, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
                                               id, P.tag, P.rk, S, Mz, tz, tid);
-          cta_reduce<NDIM, GS>(sm, S, Mz, tid);
+          cta_reduce<NDIM, GS, NT>(sm, S, Mz, tid);
         }
       }
     }  // hit < 0
@@ -681,26 +688,25 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
   if (tid == 0 && P.passes) atomicAdd(P.passes, (unsigned long long)passes);
 }
 
-// Plain passes with at most this many samples run one unit per warp (GS = 32) instead of one
-// per CTA: measured on B200.
+// Plain passes with at most this many samples run one unit per warp (GS = 32), up to
+// HJMC_QUAD_WARP_MAX_N one unit per 4 warps (GS = 128), above that one unit per CTA.
 #ifndef HJMC_WARP_UNIT_MAX_N
-#define HJMC_WARP_UNIT_MAX_N 32768
+#define HJMC_WARP_UNIT_MAX_N 4096
 #endif
 constexpr uint32_t kWarpUnitMaxN = HJMC_WARP_UNIT_MAX_N;
-// ...and only when the units alone give every SM at least this many warps (a unit per warp
-// leaves a small grid's SMs under-occupied; a 40×40 slice is better served one unit per CTA).
-#ifndef HJMC_WARP_UNIT_MIN_WARPS_PER_SM
-#define HJMC_WARP_UNIT_MIN_WARPS_PER_SM 16
-#endif
-constexpr int kWarpUnitMinWarpsPerSm = HJMC_WARP_UNIT_MIN_WARPS_PER_SM;
 
-inline int sm_count() {
-  int dev = 0, n = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-    return 148;
-  return n;
-}
+// Threads per unit of the plain kernel above HJMC_QUAD_WARP_MAX_N (the CTA by default; a
+// build variant may set 64 or 128: 4 or 2 units per CTA, synchronised by named barriers).
+#ifndef HJMC_CTA_GROUP
+#define HJMC_CTA_GROUP HJMC_NT
+#endif
+constexpr int kCtaGroup = HJMC_CTA_GROUP;
+// Plain passes with N ≤ this many samples (and above the warp switch) run 2 units per CTA
+// (GS = 128, named barriers per unit).
+#ifndef HJMC_QUAD_WARP_MAX_N
+#define HJMC_QUAD_WARP_MAX_N 65536
+#endif
+constexpr uint32_t kQuadWarpMaxN = HJMC_QUAD_WARP_MAX_N;
 
 template <class Tgt, int NDIM, int NT>
 cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
@@ -714,17 +720,24 @@ cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
   }
   if (p.proposal) {
     solve_kernel<Tgt, NDIM, NT, false, true><<<(unsigned)units, NT, 0, s>>>(p);
-  } else if (p.N <= kWarpUnitMaxN &&
-             (p.mode == kModeValueGrad ? p.M : p.M * (int64_t)p.K) >=
-                 (int64_t)kWarpUnitMinWarpsPerSm * sm_count()) {
-    // decided on the slice's full unit count, so a stepwise pass over a subset of horizons runs
-    // the same kernel (same reduction order) as the fused solve
-    constexpr int kPerCta = NT / 32;
-    const int64_t ctas = (units + kPerCta - 1) / kPerCta;
-    solve_kernel<Tgt, NDIM, NT, false, false, 32><<<(unsigned)ctas, NT, 0, s>>>(p);
-  } else {
-    solve_kernel<Tgt, NDIM, NT, false, false><<<(unsigned)units, NT, 0, s>>>(p);
+    return cudaGetLastError();
   }
+  // Threads per unit for plain passes, from N alone (measured): one warp up to
+  // N = 4,096, four warps up to N = 65,536, the CTA above. N is part of the configuration, so
+  // every shard of a slice, every subset of horizons of a stepwise pass and the fused solve run
+  // the same kernel with the same reduction order: results stay bit-identical across splits.
+  auto launch_group = [&](auto gs_tag) {
+    constexpr int GS = decltype(gs_tag)::value;
+    constexpr int kPerCta = NT / GS;
+    solve_kernel<Tgt, NDIM, NT, false, false, GS>
+        <<<(unsigned)((units + kPerCta - 1) / kPerCta), NT, 0, s>>>(p);
+  };
+  if (p.N <= kWarpUnitMaxN)
+    launch_group(std::integral_constant<int, 32>{});
+  else if (p.N <= kQuadWarpMaxN)
+    launch_group(std::integral_constant<int, 128>{});
+  else
+    launch_group(std::integral_constant<int, kCtaGroup>{});
   return cudaGetLastError();
 }
 

@@ -301,13 +301,13 @@ def test_skip_stationary_is_bit_identical():
     assert nocrn.pass_count() == M * 3 * 5
 
 
-@pytest.mark.parametrize("skip", [False, True])
-def test_reuse_passes_is_bit_identical(skip):
+@pytest.mark.parametrize("skip,N", [(False, 3000), (True, 3000), (True, 40000), (True, 70000)])
+def test_reuse_passes_is_bit_identical(skip, N):
     """HJMC_FLAG_REUSE_PASSES: under CRN a pass is a function of its c, so a pass at a c the
     unit has already used returns the stored sums. Every output equals the full schedule bit
     for bit, and the number of sample passes equals the number of distinct c per (query,
     horizon) trajectory (read off the full run's own chist), stationary skip or not."""
-    kw = dict(N=3000, K=3, Kp=8)
+    kw = dict(N=N, K=3, Kp=8)     # N picks the thread group per unit: a warp, 4 warps, the CTA
     base = Solver(SolverConfig.from_preset(I.C2, **kw))
     memo = Solver(SolverConfig.from_preset(I.C2, reuse_passes=True, skip_stationary=skip, **kw))
     x = I.queries(I.C2)[::7]
@@ -563,27 +563,25 @@ def test_binding_validates_shapes():
     s.solve_slice(x, out=s.alloc_result(10))                        # the right shapes pass
 
 
-@pytest.mark.parametrize("N", [32768, 32769])
-def test_warp_unit_and_cta_kernels_at_the_switch(O, N):
-    """Plain passes with N ≤ 32768 and ≥ 16 units per SM run one unit per warp, others one
-    unit per CTA: both kernels against the oracle at the N switch (2,400 ragged units)."""
+@pytest.mark.parametrize("N", [4096, 4097, 65536, 65537])
+def test_group_size_switches(O, N):
+    """Plain passes run one unit per warp up to N = 4096, per 4 warps up to 65536, per CTA
+    above: each kernel against the oracle on both sides of each switch (ragged 197 units)."""
     s, P = pair(O, n=3, delta=0.01, N=N, seed=I.C2.seed, system="dubins_rel", target="disk",
                 tgt_params=(5.0,))
-    M = 2400
+    M = 197
     x = I.random_queries(3, M, -9, 9, seed=N)
     cc = np.full(M, 4.0, dtype=np.float32)
     v, dv = s.value_grad(x, cc, 0.8, j_tag=3, k_tag=1, qid_base=77)
-    ids = np.arange(0, M, 7)                       # the oracle on every 7th query
+    ids = np.arange(0, M, 5)
     ref = [O.phi(P, x[i].astype(np.float64), 4.0, 0.8, qid=77 + int(i), jw=3, kw=1) for i in ids]
-    vo = np.array([r[0] for r in ref])
-    dvo = np.array([r[1] for r in ref])
-    assert_v(v.cpu().numpy()[ids], vo)
-    assert_dv(dv.cpu().numpy()[ids], dvo)
+    assert_v(v.cpu().numpy()[ids], np.array([r[0] for r in ref]))
+    assert_dv(dv.cpu().numpy()[ids], np.array([r[1] for r in ref]))
 
 
 def test_warp_unit_solve_slice_ragged(O):
     """The warp-per-unit kernel through solve_slice with a unit count that is not a multiple of
-    8 units per CTA (M·K = 2,403 ≥ 16 warps × 148 SMs)."""
+    8 units per CTA (M·K = 2,403)."""
     s, P = pair(O, n=3, delta=0.01, T=1.0, K=3, Kp=2, N=700, seed=I.C2.seed,
                 system="dubins_rel", target="disk", tgt_params=(5.0,))
     x = I.random_queries(3, 801, -9, 9, seed=5)

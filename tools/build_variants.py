@@ -9,19 +9,13 @@ from paper_2605_18566_b200 import build as B  # noqa: E402
 
 # (the warp-specialised HJMC_WS variants of an earlier revision were measured and removed)
 VARIANTS = {
-    "lgu1": ["-DHJMC_LG_UNROLL=1"],
-    "lgu2": ["-DHJMC_LG_UNROLL=2"],
-    "mb3": ["-DHJMC_MINB=3"],
-    "mb4": ["-DHJMC_MINB=4"],
-    "lg4": ["-DHJMC_LG_LANES=4"],
+    "w8k": ["-DHJMC_WARP_UNIT_MAX_N=8192"],
+    "w32k": ["-DHJMC_WARP_UNIT_MAX_N=32768"],
+    "w0": ["-DHJMC_WARP_UNIT_MAX_N=0"],
+    "q0": ["-DHJMC_WARP_UNIT_MAX_N=0", "-DHJMC_QUAD_WARP_MAX_N=0"],
+    "g128": ["-DHJMC_CTA_GROUP=128"],
     "lg2": ["-DHJMC_LG_LANES=2"],
-    "gu1": ["-DHJMC_GROUP_UNROLL=1"],
-    "gu2": ["-DHJMC_GROUP_UNROLL=2"],
-    "wu0": ["-DHJMC_WARP_UNIT_MAX_N=0"],
-    "wu64k": ["-DHJMC_WARP_UNIT_MAX_N=65536"],
-    "wuall": ["-DHJMC_WARP_UNIT_MAX_N=4294967295u"],
-    "wumin0": ["-DHJMC_WARP_UNIT_MIN_WARPS_PER_SM=0"],
-    "wumin16": ["-DHJMC_WARP_UNIT_MIN_WARPS_PER_SM=16"],
+    "mb3": ["-DHJMC_MINB=3"],
 }
 
 if __name__ == "__main__":
