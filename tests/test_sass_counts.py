@@ -57,6 +57,8 @@ def hot_loop_counts(funcs, pattern, n=None):
 
 @pytest.mark.parametrize("pattern,n,target", [
     ("DiskILi3EEELi3ELi256ELb0ELb0ELi256E", 3, "disk"),
+    ("DiskILi3EEELi3ELi256ELb0ELb0ELi128E", 3, "disk"),      # the benchmark's kernel (GS = 128)
+    ("DiskILi3EEELi3ELi256ELb0ELb0ELi32E", 3, "disk"),       # one unit per warp
     ("RelDisk6ILi6EEELi6ELi256ELb0ELb0ELi256E", 6, "rel_disk6"),
     ("PairUnionILi15EEELi15ELi256ELb0ELb0ELi256E", 15, "pair_union"),
 ])
