@@ -15,8 +15,16 @@
  *   orc_phi             pinned: constant/linear/quadratic closed forms, Gauss–Hermite and
  *                       noncentral-χ² quadrature, Jensen bounds, shift/translation identities
  *   orc_solve_slice     pinned: quadratic CRN stationarity, tube ≤ g and ≤ every v_j,
- *                       per-sample BRT band bound; every step is orc_phi + orc_gamma
+ *                       per-sample BRT band bound; every step is orc_phi + orc_gamma; the MC
+ *                       Picard reproduces a Gauss–Hermite-quadrature Picard on clamped queries
+ *   orc_avoid_l         pinned: BRAT clamp identities (disk obstacle)
+ *   orc_picard_adaptive pinned: equals the fixed schedule at tol = 0, stops at the first
+ *                       ε < tol (Algorithm 1 step 5); SPEC's contraction example
  *   orc_residual_partials  pinned: hand-computable small arrays
+ *   (Laplace proposal mode of orc_phi) pinned: zero variance on linear g, closed form and ESS
+ *                       gain on the quadratic bowl, agreement with the plain estimator
+ * Parity unpinned: end-to-end BRT accuracy against the true inviscid value (needs grid
+ * reference solutions the paper used, P:469 — not available).
  */
 #ifndef HJMC_ORACLE_H_
 #define HJMC_ORACLE_H_
