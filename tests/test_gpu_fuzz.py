@@ -1,0 +1,60 @@
+"""Seeded random parity sweep: value_grad through every kernel variant (one unit per warp / per
+4 warps / per CTA, lane groups, antithetic, Laplace proposal) on random targets, dimensions,
+sample counts, coefficients, horizons and query sets — GPU vs the oracle at the R20 tolerances.
+Deterministic (fixed generator seed): a failure names its case index and parameters."""
+import numpy as np
+import pytest
+
+from _parity import assert_dv, assert_v
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2605_18566_b200 import inputs as I  # noqa: E402
+from paper_2605_18566_b200.solver import Solver, SolverConfig  # noqa: E402
+
+# (target, n, target params, system, coordinate range)
+TARGETS = [
+    ("disk", 2, (1.0,), "quadratic", 3.0),
+    ("disk", 3, (5.0,), "dubins_rel", 12.0),
+    ("rel_disk6", 6, (1.5,), "rocket6", 6.0),
+    ("pair_union", 15, (1.0,), "dubins_pairs", 5.0),
+    ("pair_union", 45, (1.0,), "dubins_pairs", 5.0),
+    ("pursuit_min", 45, (1.5,), "multiagent", 6.0),
+    ("quad_bowl", 2, (0.25,), "quadratic", 1.0),
+    ("linear", 4, (0.5, -1.0, 2.0, 0.3, 0.1), "quadratic", 2.0),
+]
+N_CHOICES = [1, 6, 257, 4096, 4097, 9001, 65536, 65537]
+
+
+def cases(count=24, seed=20261020):
+    rng = np.random.default_rng(seed)
+    for i in range(count):
+        tgt, n, prm, sysname, span = TARGETS[i % len(TARGETS)]
+        N = int(rng.choice(N_CHOICES if n < 40 else [7, 4097, 9001]))
+        yield i, dict(target=tgt, n=n, tgt_params=prm[: max(1, n + 1)] if tgt == "linear" else prm,
+                      system=sysname, span=span, N=N, M=int(rng.integers(1, 40)),
+                      c=float(np.exp(rng.uniform(np.log(0.05), np.log(20.0)))),
+                      tau=float(rng.uniform(0.05, 1.0)), antithetic=bool(rng.random() < 0.25),
+                      proposal="laplace" if rng.random() < 0.2 else "plain",
+                      seed=int(rng.integers(0, 2**62)), qid_base=int(rng.integers(0, 2**31)))
+
+
+@pytest.mark.parametrize("i,case", list(cases()))
+def test_random_value_grad_parity(oracle_mod, i, case):
+    O = oracle_mod
+    kw = dict(n=case["n"], delta=0.01, N=case["N"], seed=case["seed"], system=case["system"],
+              target=case["target"], tgt_params=case["tgt_params"], antithetic=case["antithetic"],
+              proposal=case["proposal"])
+    s = Solver(SolverConfig(**kw))
+    P = O.Problem(**kw)
+    x = I.random_queries(case["n"], case["M"], -case["span"], case["span"], seed=i)
+    cc = np.full(case["M"], case["c"], dtype=np.float32)
+    v, dv = s.value_grad(x, cc, case["tau"], j_tag=i + 1, k_tag=i % 7, qid_base=case["qid_base"])
+    vo, dvo = O.phi_batch(P, x, cc.astype(np.float64), case["tau"], qid_base=case["qid_base"],
+                          jw=i + 1, kw=i % 7)
+    assert_v(v.cpu().numpy(), vo, f"case {i} {case}")
+    assert_dv(dv.cpu().numpy(), dvo, f"case {i} {case}")

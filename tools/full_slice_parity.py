@@ -64,6 +64,24 @@ def main(name="c2"):
                 propagated_ok += 1
             else:
                 failed.append([int(m), int(j)])
+    # final outputs (v, Dv, tube at τ_K) as tests/test_gpu_parity.py::_final_outputs_within:
+    # R20, else the propagated bound of the last horizon's trajectory
+    okv = v_violations(out["v"], ref["v"]) <= 1.0
+    okd = dv_violations(out["dv"], ref["dv"]) <= 1.0
+    okt = v_violations(out["tube"], ref["tube"]) <= 1.0
+    final_plain = int(np.sum(okv & okd & okt))
+    final_prop, final_failed = 0, []
+    for m in np.flatnonzero(~(okv & okd & okt)):
+        bv, _, bd = propagated_bounds(O, P, xd[m], m, p.K, ref["chist"][-1, :, m],
+                                      ref["vhist"][-1, :, m], ref["dvhist"][-1, :, m], floor)
+        if (abs(out["v"][m] - ref["v"][m]) <= bv[-1]
+                and np.linalg.norm(out["dv"][m] - ref["dv"][m]) <= bd[-1]):
+            final_prop += 1
+        else:
+            final_failed.append(int(m))
+    if os.environ.get("HJMC_PARITY_DUMP"):
+        np.savez_compressed(os.environ["HJMC_PARITY_DUMP"], **{f"gpu_{k}": v for k, v in out.items()},
+                            **{f"ref_{k}": v for k, v in ref.items() if k != "status"})
     last = (np.abs(ref["chist"][-1, -1] - out["chist"][-1, -1]) > 0)
     rep = {
         "config": p.name, "queries": M, "units": M * p.K, "iterates_per_unit": p.Kp,
@@ -72,6 +90,9 @@ def main(name="c2"):
         "units_within_propagated_bound": propagated_ok,
         "units_failed": len(failed), "failed": failed[:20],
         "worst_vhist_ratio_plain_units": round(float(worst_plain), 4),
+        "final_outputs_within_plain_tolerances": final_plain,
+        "final_outputs_within_propagated_bound": final_prop,
+        "final_outputs_failed": final_failed[:20],
         "worst_ratio_final": {
             "v": round(float(v_violations(out["v"], ref["v"]).max()), 4),
             "dv": round(float(dv_violations(out["dv"], ref["dv"]).max()), 4),
