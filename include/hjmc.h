@@ -111,7 +111,9 @@
  *    With cfg.flags & HJMC_FLAG_SYNC_CHECK every device entry point synchronises and returns
  *    HJMC_ENUMERIC itself.
  *  * Results are a pure function of (config, system, target, x, drift, global query ids):
- *    independent of M, of how queries are split across calls or GPUs, and of the grid shape.
+ *    independent of M, of how queries are split across calls or GPUs, and of the grid shape —
+ *    bit for bit: the kernel variant (threads per (query, horizon) unit, hence the reduction
+ *    order) is chosen from the configuration (N, n, target, antithetic, proposal) only.
  *  * A handle is not thread-safe; use one per host thread / stream. No C++ exception crosses
  *    the ABI. hjmc_last_error() returns a human-readable message for the last failure.
  */
