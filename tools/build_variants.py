@@ -16,6 +16,9 @@ VARIANTS = {
     "g128": ["-DHJMC_CTA_GROUP=128"],
     "lg2": ["-DHJMC_LG_LANES=2"],
     "mb3": ["-DHJMC_MINB=3"],
+    "mb4": ["-DHJMC_MINB=4"],
+    "mb5": ["-DHJMC_MINB=5"],
+    "mb6": ["-DHJMC_MINB=6"],
 }
 
 if __name__ == "__main__":
