@@ -577,7 +577,10 @@ int hjmc_picard_solve(hjmc_handle* h, const float* x, const uint32_t* qid, uint3
   const std::vector<uintptr_t> key = {
       (uintptr_t)x, (uintptr_t)qid, qid_base, (uintptr_t)M, (uintptr_t)drift, tol_key,
       (uintptr_t)max_iter, (uintptr_t)v, (uintptr_t)dv, (uintptr_t)c, (uintptr_t)iters,
-      (uintptr_t)eps, (uintptr_t)dsup, h->generation};
+      (uintptr_t)eps, (uintptr_t)dsup, h->generation,
+      // handle scratch the graph reads: another entry point may have reallocated it since
+      (uintptr_t)h->d_cstate, (uintptr_t)h->d_vprev, (uintptr_t)h->d_partial,
+      (uintptr_t)h->d_pstate};
   cudaError_t e;
   if (realloc || !h->pic_exec || key != h->pic_key) {
     if (h->pic_exec) cudaGraphExecDestroy(h->pic_exec);

@@ -615,6 +615,10 @@ def test_picard_device_resident_equals_host_driven(O, crn):
     b3 = solve_adaptive_device(s, x, tol=0.0, max_iter=3)
     assert list(b3["iters"]) == [3, 3, 3]
     np.testing.assert_array_equal(b3["eps"][:, :3], r0["eps"][:, :3])
+    # a larger host-driven solve reallocates the handle's scratch: the cached graph must notice
+    solve_adaptive(s, I.queries(p)[::5], tol=0.0, max_iter=2)
+    b4 = solve_adaptive_device(s, x, tol=tol, max_iter=6)
+    assert torch.equal(b["v"], b4["v"]) and list(b["iters"]) == list(b4["iters"])
     # an exactly stationary problem stops after the second pass (quadratic H, CRN: c = 1/δ)
     q = Solver(SolverConfig(n=2, delta=0.05, T=0.5, K=2, N=2048, system="quadratic",
                             target="quad_bowl", tgt_params=(0.25,)))
