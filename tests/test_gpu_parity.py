@@ -203,16 +203,24 @@ def test_picard_quadratic_crn_stationary_gpu(O):
         np.testing.assert_allclose(g["vhist"][:, k], g["vhist"][:, 0], rtol=1e-6, atol=1e-7)
 
 
-def test_shard_bit_identity():
-    """Results depend on global query ids only: any split of the queries is bit-identical."""
-    s = Solver(SolverConfig.from_preset(I.C2, N=3000, K=2, Kp=2))
-    x = I.queries(I.C2)[:500]
+@pytest.mark.parametrize("N", [3000, 20000, 70000])    # one unit per warp / 4 warps / CTA
+def test_shard_bit_identity(N):
+    """Results depend on global query ids only: the 1/2/4/8-GPU partitions of shard.partition
+    and a ragged hand split are bit-identical to the unsplit slice, for every thread-group
+    size (the kernel variant depends on N only)."""
+    from paper_2605_18566_b200 import shard
+
+    s = Solver(SolverConfig.from_preset(I.C2, N=N, K=2, Kp=2))
+    x = I.queries(I.C2)[:501]
     full = s.solve_slice(x)
-    a = s.solve_slice(x[:123], qid_base=0)
-    b = s.solve_slice(x[123:], qid_base=123)
-    for k in ("v", "dv", "c", "tube"):
-        assert torch.equal(full[k], torch.cat([a[k], b[k]]))
-    assert torch.equal(full["vhist"], torch.cat([a["vhist"], b["vhist"]], dim=2))
+    splits = [[(0, 123), (123, 378)]]
+    for world in (2, 4, 8):
+        splits.append([shard.partition(501, world, r) for r in range(world)])
+    for parts in splits:
+        outs = [s.solve_slice(x[a:a + n], qid_base=a) for a, n in parts]
+        for k in ("v", "dv", "c", "tube"):
+            assert torch.equal(full[k], torch.cat([o[k] for o in outs])), (parts, k)
+        assert torch.equal(full["vhist"], torch.cat([o["vhist"] for o in outs], dim=2))
 
 
 def test_host_path_matches_device_path():
@@ -624,3 +632,18 @@ def test_picard_device_resident_equals_host_driven(O, crn):
                             target="quad_bowl", tgt_params=(0.25,)))
     rq = solve_adaptive_device(q, I.queries(I.C1)[::9], tol=1e-9, max_iter=10)
     assert list(rq["iters"]) == [2, 2] and np.all(rq["eps"][:, 1] == 0.0)
+
+
+def test_shard_bit_identity_lane_groups():
+    """The n = 45 lane-group kernel: the 4-GPU partition is bit-identical to the unsplit slice."""
+    from paper_2605_18566_b200 import shard
+
+    p = I.C5.with_(N=3000, K=2, Kp=2, grid_pts=8)
+    s = Solver(SolverConfig.from_preset(p))
+    x = I.queries(p)[:301]
+    full = s.solve_slice(x)
+    outs = [s.solve_slice(x[a:a + n], qid_base=a) for a, n in
+            (shard.partition(301, 4, r) for r in range(4))]
+    for k in ("v", "dv", "c", "tube", "vhist"):
+        dim = 2 if k == "vhist" else 0
+        assert torch.equal(full[k], torch.cat([o[k] for o in outs], dim=dim)), k
