@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 import oracle as O  # noqa: E402
 from paper_2605_18566_b200 import inputs as I  # noqa: E402
 
-COUNTS = {3: (12, 6, 6), 4: (6, 3, 3), 5: (4, 2, 2)}
+COUNTS = {3: (256, 64, 64), 4: (64, 16, 16), 5: (24, 8, 8)}
 
 
 def sample_ids(p, P, x, n_spread, n_band, n_int):
