@@ -1,15 +1,19 @@
 // hjmc_solve_impl.cuh — the fused Monte-Carlo Picard kernel (SURVEY §8(a) rows a1–a11).
 //
-// One CTA owns one work unit = (query m, horizon j) and runs the whole Picard loop of that
-// horizon (Algorithm 1) without leaving the SM: queries and horizons are mutually
+// A group of threads — one warp, four warps or the whole CTA, chosen from N (launch_solve) —
+// owns one work unit = (query m, horizon j) and runs the whole Picard loop of that horizon
+// (Algorithm 1) without leaving the SM: queries and horizons are mutually
 // independent (R5, R9), so no grid-wide synchronisation or inter-CTA traffic exists.
 // Per Picard iterate (one Φ pass):
 //   every thread walks a strided subset of the N samples; per sample it regenerates its
 //   normals from Philox in registers (no sample array in memory), forms y = x + σz, evaluates
 //   g, and accumulates w = 2^(A·core + B) and w·z (A = −c log2 e; B a guaranteed-safe shift,
 //   hjmc_targets.cuh) — one FFMA + one MUFU.EX2 per weight, no per-sample max or rescale;
-//   then a warp-shuffle butterfly and a shared-memory merge across warps give the CTA sums,
-//   and thread 0 forms v, Dv and the next frozen coefficient c = Γ(x, Dv) in double.
+//   then a warp-shuffle butterfly and a shared-memory merge across the group's warps give the
+//   unit's sums, and the group's thread 0 forms v, Dv and the next frozen coefficient
+//   c = Γ(x, Dv) in double. For n = 37–48 pair-min targets a sample is spread over a lane
+//   group instead (lg_pass), and under CRN a pass at an already-used c is not re-sampled
+//   (HJMC_FLAG_REUSE_PASSES).
 #pragma once
 #include <cuda_runtime.h>
 
