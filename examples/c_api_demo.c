@@ -88,14 +88,38 @@ int main(void) {
   }
   uint64_t passes = 0;
   CHECK(hjmc_pass_count(h, NULL, &passes));
+
+  /* Algorithm 1 on the device: Kp passes, tol = 0 → the last horizon's v equals the fixed
+   * schedule's v (same counters, same kernels) */
+  const int K = cfg.K, Kp = cfg.Kp;
+  float *pv, *pc;
+  int32_t* piters;
+  double *peps, *pdsup;
+  cudaMalloc((void**)&pv, sizeof(float) * K * M);
+  cudaMalloc((void**)&pc, sizeof(float) * K * M);
+  cudaMalloc((void**)&piters, sizeof(int32_t) * K);
+  cudaMalloc((void**)&peps, sizeof(double) * K * Kp);
+  cudaMalloc((void**)&pdsup, sizeof(double) * K * Kp);
+  CHECK(hjmc_picard_solve(h, dx, NULL, 0, M, NULL, 0.0, Kp, pv, NULL, pc, piters, peps, pdsup,
+                          NULL));
+  cudaDeviceSynchronize();
+  float* v3 = (float*)malloc(sizeof(float) * M);
+  int32_t iters[64];
+  double eps_last = 0.0;
+  cudaMemcpy(v3, pv + (size_t)(K - 1) * M, sizeof(float) * M, cudaMemcpyDeviceToHost);
+  cudaMemcpy(iters, piters, sizeof(int32_t) * K, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&eps_last, peps + (size_t)(K - 1) * Kp + (Kp - 1), sizeof(double), cudaMemcpyDeviceToHost);
+  int picard_same = memcmp(v1, v3, sizeof(float) * M) == 0 && iters[K - 1] == Kp;
   printf("{\"version\": %d, \"M\": %lld, \"identical_device_host\": %s, \"brt_points\": %d, "
-         "\"v_min\": %.6f, \"v_max\": %.6f, \"passes\": %llu}\n",
+         "\"v_min\": %.6f, \"v_max\": %.6f, \"passes\": %llu, "
+         "\"picard_graph_matches_fixed_schedule\": %s, \"eps_last\": %.6g}\n",
          hjmc_version(), (long long)M, same ? "true" : "false", inside, vmin, vmax,
-         (unsigned long long)passes);
+         (unsigned long long)passes, picard_same ? "true" : "false", eps_last);
   hjmc_destroy(h);
   cudaFree(dx);
   cudaFree(dv);
   cudaFree(dtube);
-  free(x); free(v1); free(t1); free(v2); free(t2);
-  return same ? 0 : 2;
+  cudaFree(pv); cudaFree(pc); cudaFree(piters); cudaFree(peps); cudaFree(pdsup);
+  free(x); free(v1); free(t1); free(v2); free(t2); free(v3);
+  return (same && picard_same) ? 0 : 2;
 }

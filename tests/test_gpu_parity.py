@@ -483,6 +483,7 @@ def test_plain_c_consumer(tmp_path):
     assert rec["identical_device_host"] and rec["M"] == 441
     assert rec["passes"] == 2 * 441 * 4 * 3       # device + host solve, full schedule
     assert rec["brt_points"] > 0
+    assert rec["picard_graph_matches_fixed_schedule"]
 
 
 def test_counter_extremes(O):
