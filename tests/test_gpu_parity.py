@@ -650,3 +650,25 @@ def test_shard_bit_identity_lane_groups():
     for k in ("v", "dv", "c", "tube", "vhist"):
         dim = 2 if k == "vhist" else 0
         assert torch.equal(full[k], torch.cat([o[k] for o in outs], dim=dim)), k
+
+
+@pytest.mark.parametrize("target,n,params,system,extra", [
+    ("disk", 3, (5.0,), "dubins_rel", {}),
+    ("pair_union", 45, (1.0,), "dubins_pairs", {}),                       # lane groups
+    ("disk", 3, (5.0,), "dubins_rel", {"proposal": "laplace"}),
+    ("rel_disk6", 6, (1.5,), "rocket6", {"antithetic": True}),
+])
+def test_solve_slice_with_drift_vs_oracle(O, target, n, params, system, extra):
+    """The optional drift hook (R4: y = x + bτ + σz, b per query) through the fused solve —
+    generic, lane-group, Laplace-proposal and antithetic kernels — against the oracle at every
+    Picard iterate (the translation identity alone would not catch a drift applied with the
+    wrong τ_j)."""
+    s, P = pair(O, n=n, delta=0.01, T=1.0, K=3, Kp=3, N=1500, seed=77, system=system,
+                target=target, tgt_params=params, **extra)
+    x = I.random_queries(n, 29, -6, 6, seed=n + 5)
+    b = I.random_queries(n, 29, -2, 2, seed=n + 6)
+    out = s.solve_slice(x, qid_base=9, drift=b)
+    ref = O.solve_slice(P, x, drift=b, qid_base=9)
+    assert ref["status"] == 0
+    g = {k: t.cpu().numpy() for k, t in out.items()}
+    assert_picard_history(O, P, x, np.arange(29) + 9, g["vhist"], g["chist"], ref)
