@@ -1,6 +1,7 @@
 """Seeded random parity sweep: value_grad through every kernel variant (one unit per warp / per
 4 warps / per CTA, lane groups, antithetic, Laplace proposal) on random targets, dimensions,
-sample counts, coefficients, horizons and query sets — GPU vs the oracle at the R20 tolerances.
+sample counts, coefficients, horizons, viscosities (both conventions, R1) and query sets — GPU
+vs the oracle at the R20 tolerances.
 Deterministic (fixed generator seed): a failure names its case index and parameters."""
 import numpy as np
 import pytest
@@ -40,13 +41,16 @@ def cases(count=24, seed=20261020):
                       c=float(np.exp(rng.uniform(np.log(0.05), np.log(20.0)))),
                       tau=float(rng.uniform(0.05, 1.0)), antithetic=bool(rng.random() < 0.25),
                       proposal="laplace" if rng.random() < 0.2 else "plain",
-                      seed=int(rng.integers(0, 2**62)), qid_base=int(rng.integers(0, 2**31)))
+                      seed=int(rng.integers(0, 2**62)), qid_base=int(rng.integers(0, 2**31)),
+                      delta=float(np.exp(rng.uniform(np.log(0.005), np.log(0.1)))),
+                      visc="full" if rng.random() < 0.3 else "paper")
 
 
 @pytest.mark.parametrize("i,case", list(cases()))
 def test_random_value_grad_parity(oracle_mod, i, case):
     O = oracle_mod
-    kw = dict(n=case["n"], delta=0.01, N=case["N"], seed=case["seed"], system=case["system"],
+    kw = dict(n=case["n"], delta=case["delta"], visc=case["visc"], N=case["N"], seed=case["seed"],
+              system=case["system"],
               target=case["target"], tgt_params=case["tgt_params"], antithetic=case["antithetic"],
               proposal=case["proposal"])
     s = Solver(SolverConfig(**kw))
