@@ -43,7 +43,7 @@ res = solve_adaptive(solver, x, tol=1e-4, max_iter=15, log=records.append)
 for r in records:
     print(json.dumps({k: (round(v, 6) if isinstance(v, float) else v) for k, v in r.items()
                       if k in ("k", "ms", "max_abs_v", "c_min", "c_max")}))
-print("iterations per horizon:", list(res["iters"]))
+print("iterations per horizon:", [int(i) for i in res["iters"]])
 rep = ContractionReport.from_differences(res["d_sup"][-1][: res["iters"][-1]])
 print("empirical contraction ratios q̂ (last horizon):", np.round(rep.q_hat, 4).tolist())
 
@@ -51,4 +51,4 @@ print("empirical contraction ratios q̂ (last horizon):", np.round(rep.q_hat, 4)
 t0 = time.perf_counter()
 dev = solve_adaptive_device(solver, x, tol=1e-4, max_iter=15)
 print(f"device-graph Algorithm 1: {time.perf_counter() - t0:.3f} s, iterations per horizon "
-      f"{list(dev['iters'])}, identical v: {bool((dev['v'] == res['v']).all())}")
+      f"{[int(i) for i in dev['iters']]}, identical v: {bool((dev['v'] == res['v']).all())}")
