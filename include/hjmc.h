@@ -161,6 +161,12 @@ extern "C" {
  * between the clamps c_min ↔ c_max that dominate the game slices (R8, R27). Outputs are
  * identical with and without the flag; hjmc_pass_count() reports the sample passes run. */
 #define HJMC_FLAG_REUSE_PASSES 4u
+/* With HJMC_FLAG_REUSE_PASSES and crn = 1, for n ≤ 6 and the plain proposal without antithetic
+ * sampling: a pass whose frozen c sits on a clamp (c_min or c_max) also accumulates, from the
+ * same samples, the sums at the opposite clamp and memoizes them (when they need no two-pass
+ * fallback), so a c_min ↔ c_max Picard 2-cycle costs one sampling pass. Outputs are identical
+ * with and without the flag; ignored where it does not apply. */
+#define HJMC_FLAG_SPECULATE_CLAMPS 8u
 
 /* Sampling proposal of a Φ pass (reading R28).
  *  PLAIN:   y_i = x + bτ + σ z_i — the estimator of Cor. logsumexp / mc_gradient.

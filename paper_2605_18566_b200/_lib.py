@@ -22,6 +22,7 @@ VISC = {"paper": 0, "full": 1}
 FLAG_SYNC_CHECK = 1
 FLAG_SKIP_STATIONARY = 2
 FLAG_REUSE_PASSES = 4
+FLAG_SPECULATE_CLAMPS = 8
 PROPOSALS = {"plain": 0, "laplace": 1}
 
 EXPORTS = [

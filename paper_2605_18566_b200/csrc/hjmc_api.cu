@@ -116,6 +116,7 @@ void fill_common(const hjmc_handle* h, SolveParams* p) {
   p->bad = h->d_bad;
   p->skip_stationary = (h->cfg.flags & HJMC_FLAG_SKIP_STATIONARY) ? 1 : 0;
   p->reuse_passes = (h->cfg.flags & HJMC_FLAG_REUSE_PASSES) ? 1 : 0;
+  p->speculate = (h->cfg.flags & HJMC_FLAG_SPECULATE_CLAMPS) ? 1 : 0;
   p->passes = h->d_passes;
 }
 
@@ -180,7 +181,8 @@ int hjmc_create(const hjmc_config* cfg, hjmc_handle** out) {
   if (c.antithetic != 0 && c.antithetic != 1) return fail(nullptr, HJMC_EINVAL, "antithetic must be 0 or 1");
   if (c.proposal != HJMC_PROPOSAL_PLAIN && c.proposal != HJMC_PROPOSAL_LAPLACE)
     return fail(nullptr, HJMC_EINVAL, "proposal must be PLAIN or LAPLACE");
-  if (c.flags & ~(HJMC_FLAG_SYNC_CHECK | HJMC_FLAG_SKIP_STATIONARY | HJMC_FLAG_REUSE_PASSES))
+  if (c.flags & ~(HJMC_FLAG_SYNC_CHECK | HJMC_FLAG_SKIP_STATIONARY | HJMC_FLAG_REUSE_PASSES |
+                  HJMC_FLAG_SPECULATE_CLAMPS))
     return fail(nullptr, HJMC_EINVAL, "unknown flag bits");
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);

@@ -42,6 +42,7 @@ struct SolveParams {
   unsigned long long* bad;
   int skip_stationary;             // HJMC_FLAG_SKIP_STATIONARY
   int reuse_passes;                // HJMC_FLAG_REUSE_PASSES
+  int speculate;                   // HJMC_FLAG_SPECULATE_CLAMPS
   unsigned long long* passes;      // Φ passes executed (accounting), nullable
   // stepwise Picard (kModePass): one pass per (query, active horizon)
   double* c_state;                 // [K][M] frozen coefficient in, Γ(x, Dv) out

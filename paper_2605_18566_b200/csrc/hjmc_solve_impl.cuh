@@ -59,15 +59,30 @@ __device__ __forceinline__ float warp_max(float v) {
 // Samples are walked in draw groups (R19, DrawLayout): a thread generates the group's normal
 // stream (Q Philox blocks) and then runs its G samples; groups are strided over the CTA.
 // kTilt (Laplace proposal, R28): the log2 weight gains the likelihood-ratio term sgn·(tz·ẑ).
-template <class Tgt, int NDIM, bool kTilt>
+// Speculative second weight (HJMC_FLAG_SPECULATE_CLAMPS): the same sample's sums at another
+// frozen coefficient c' — w' = 2^(A'·core + B') — accumulated alongside (same core, same order).
+template <int NDIM>
+struct SpecSums {
+  float A, B, S, Mz[NDIM];
+};
+
+template <class Tgt, int NDIM, bool kTilt, bool kSpec = false>
 __device__ __forceinline__ void accumulate_sample(const Tgt& tgt, const float (&xs)[NDIM],
                                                   float sigma, float A, float B,
                                                   const float (&tz)[NDIM], const float* zg,
-                                                  float sgn, float& S, float (&Mz)[NDIM]) {
+                                                  float sgn, float& S, float (&Mz)[NDIM],
+                                                  SpecSums<NDIM>* sp = nullptr) {
   float z[NDIM];
 #pragma unroll
   for (int d = 0; d < NDIM; ++d) z[d] = zg[d];
-  float a = fmaf(A, tgt.core(xs, sgn * sigma, z), B);
+  const float core_v = tgt.core(xs, sgn * sigma, z);
+  float a = fmaf(A, core_v, B);
+  if constexpr (kSpec) {
+    const float w2 = ex2_approx(fmaf(sp->A, core_v, sp->B));
+    sp->S += w2;
+#pragma unroll
+    for (int d = 0; d < NDIM; ++d) sp->Mz[d] = fmaf(w2, z[d], sp->Mz[d]);
+  }
   if constexpr (kTilt) {
     float t = 0.f;
 #pragma unroll
@@ -83,13 +98,14 @@ __device__ __forceinline__ void accumulate_sample(const Tgt& tgt, const float (&
 
 // NT here is the size of the thread group that shares one unit (the CTA, or one warp in the
 // warp-per-unit kernel) and tid the thread's index in it.
-template <class Tgt, int NDIM, int NT, bool kTilt = false>
+template <class Tgt, int NDIM, int NT, bool kTilt = false, bool kSpec = false>
 __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[NDIM],
                                                    float sigma, float A, float B, uint32_t N,
                                                    int antithetic, uint32_t w1base, uint32_t qid,
                                                    uint32_t tag, const RoundKeys& rk, float& S,
                                                    float (&Mz)[NDIM], const float (&tz)[NDIM],
-                                                   uint32_t tid) {
+                                                   uint32_t tid, SpecSums<NDIM>* sp = nullptr) {
+  static_assert(!(kSpec && kTilt), "speculation only for the plain proposal");
   using L = DrawLayout<NDIM>;
   S = 0.f;
 #pragma unroll
@@ -104,7 +120,8 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
       group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
 #pragma unroll
       for (int r = 0; r < L::G; ++r)
-        accumulate_sample<Tgt, NDIM, kTilt>(tgt, xs, sigma, A, B, tz, zz + r * NDIM, 1.f, S, Mz);
+        accumulate_sample<Tgt, NDIM, kTilt, kSpec>(tgt, xs, sigma, A, B, tz, zz + r * NDIM, 1.f, S,
+                                                   Mz, sp);
     }
     for (uint32_t g = full + tid; g < groups; g += NT) {  // ragged tail group
       float zz[L::L];
@@ -112,7 +129,8 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
 #pragma unroll
       for (int r = 0; r < L::G; ++r)
         if (g * L::G + r < N)
-          accumulate_sample<Tgt, NDIM, kTilt>(tgt, xs, sigma, A, B, tz, zz + r * NDIM, 1.f, S, Mz);
+          accumulate_sample<Tgt, NDIM, kTilt, kSpec>(tgt, xs, sigma, A, B, tz, zz + r * NDIM, 1.f,
+                                                     S, Mz, sp);
     }
   } else {
     for (uint32_t g = tid; g < groups; g += NT) {
@@ -172,6 +190,7 @@ template <int NDIM, int NT>
 struct SolveSmem {
   float part[NT / 32][NDIM + 1];
   double sum[NDIM + 1];
+  double sum2[NDIM + 1];  // speculative pass sums (HJMC_FLAG_SPECULATE_CLAMPS)
   double memo_sum[kMemo][NDIM + 1];
   double memo_c[kMemo];
   float memo_B[kMemo];
@@ -197,16 +216,17 @@ __device__ __forceinline__ void group_sync() {
 // size: the CTA or a part of it (shared-memory merge across its warps) or one warp (shuffles).
 template <int NDIM, int NT, int CTA = NT>
 __device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, float (&Mz)[NDIM],
-                                           uint32_t tid) {
+                                           uint32_t tid, double* dst = nullptr) {
+  double* out = dst ? dst : sm.sum;
   const int lane = tid & 31, warp = tid >> 5;
   S = warp_sum(S);
 #pragma unroll
   for (int d = 0; d < NDIM; ++d) Mz[d] = warp_sum(Mz[d]);
   if constexpr (NT == 32) {
     if (lane == 0) {
-      sm.sum[0] = (double)S;
+      out[0] = (double)S;
 #pragma unroll
-      for (int d = 0; d < NDIM; ++d) sm.sum[1 + d] = (double)Mz[d];
+      for (int d = 0; d < NDIM; ++d) out[1 + d] = (double)Mz[d];
     }
     __syncwarp();
     return;
@@ -221,7 +241,7 @@ __device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, flo
     double acc = 0.0;
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) acc += (double)sm.part[w][col];
-    sm.sum[col] = acc;
+    out[col] = acc;
   }
   group_sync<NT, CTA>();
 }
@@ -489,7 +509,11 @@ constexpr int min_blocks() {
 // kernel for small N, where a CTA-wide unit would spend most of its time in the per-pass
 // reduction, barriers and thread-0 epilogue; with one unit per warp those latencies of one
 // unit overlap the sampling of the CTA's other seven, and no __syncthreads exists).
-template <class Tgt, int NDIM, int NT, bool kLG = false, bool kProp = false, int GS = NT>
+// kSpec (HJMC_FLAG_SPECULATE_CLAMPS, plain passes, n ≤ 6): while sampling at c, also
+// accumulate the sums at the opposite clamp (c_max ↔ c_min) and memoize them, so a Picard
+// 2-cycle between the clamps costs one sampling pass instead of two.
+template <class Tgt, int NDIM, int NT, bool kLG = false, bool kProp = false, int GS = NT,
+          bool kSpec = false>
 __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(const __grid_constant__ SolveParams P) {
   static_assert(GS == NT || (!kLG && GS >= 32 && NT % GS == 0 && GS % 32 == 0),
                 "thread groups smaller than the CTA only for the generic kernel");
@@ -615,6 +639,18 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
           hit = e;
           break;
         }
+    // speculation target: the opposite clamp, if not memoized yet and the memo has room for both
+    double c_spec = 0.0;
+    float B_spec = 0.f;
+    bool do_spec = false;
+    if constexpr (kSpec) {
+      if (memo_on && hit < 0) {
+        c_spec = (c == P.gp.c_max) ? P.gp.c_min : ((c == P.gp.c_min) ? P.gp.c_max : 0.0);
+        do_spec = c_spec != 0.0 && sm.n_memo + 2 <= kMemo;
+        for (int e = 0; e < sm.n_memo; ++e)
+          if (sm.memo_c[e] == c_spec) do_spec = false;
+      }
+    }
     if (hit < 0) {
       if constexpr (kLG) {
         float S, Mb[kLgSpan], amax;
@@ -622,9 +658,29 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
         lg_reduce<NDIM, NT>(sm, S, Mb);
       } else {
         float S, Mz[NDIM];
-        mc_accumulate<Tgt, NDIM, GS, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base, id,
-                                            P.tag, P.rk, S, Mz, tz, tid);
-        cta_reduce<NDIM, GS, NT>(sm, S, Mz, tid);
+        bool plain = true;
+        if constexpr (kSpec) {
+          if (do_spec) {
+            // exactly the A and B a pass at c_spec would use (tilt 0: plain proposal)
+            SpecSums<NDIM> sp;
+            sp.A = opaque((float)(-c_spec * kLog2e));
+            sp.B = opaque(-sp.A * tgt.core_lower(ctr, sigma) - 0.f);
+            sp.S = 0.f;
+#pragma unroll
+            for (int d = 0; d < NDIM; ++d) sp.Mz[d] = 0.f;
+            mc_accumulate<Tgt, NDIM, GS, false, true>(tgt, ctr, sigma_s, A, B, P.N, 0, w1base, id,
+                                                      P.tag, P.rk, S, Mz, tz, tid, &sp);
+            cta_reduce<NDIM, GS, NT>(sm, S, Mz, tid);
+            cta_reduce<NDIM, GS, NT>(sm, sp.S, sp.Mz, tid, sm.sum2);
+            B_spec = sp.B;
+            plain = false;
+          }
+        }
+        if (plain) {
+          mc_accumulate<Tgt, NDIM, GS, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
+                                              id, P.tag, P.rk, S, Mz, tz, tid);
+          cta_reduce<NDIM, GS, NT>(sm, S, Mz, tid);
+        }
       }
       if (!(sm.sum[0] >= (double)kUnderflowS)) {
         // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with
@@ -671,6 +727,15 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
           sm.memo_c[e] = c;
           sm.memo_B[e] = B;
           for (int d = 0; d <= NDIM; ++d) sm.memo_sum[e][d] = sm.sum[d];
+          sm.n_memo = e + 1;
+        }
+        // a speculative sum is kept only when a real pass at c_spec would not have needed the
+        // two-pass fallback (same S, same threshold): then it equals that pass bit for bit
+        if (do_spec && sm.sum2[0] >= (double)kUnderflowS && sm.n_memo < kMemo) {
+          const int e = sm.n_memo;
+          sm.memo_c[e] = c_spec;
+          sm.memo_B[e] = B_spec;
+          for (int d = 0; d <= NDIM; ++d) sm.memo_sum[e][d] = sm.sum2[d];
           sm.n_memo = e + 1;
         }
       }
@@ -736,6 +801,27 @@ cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
     solve_kernel<Tgt, NDIM, NT, false, false, GS>
         <<<(unsigned)((units + kPerCta - 1) / kPerCta), NT, 0, s>>>(p);
   };
+  // (the bowl, linear and constant targets never cycle between clamps: no speculative variant)
+  constexpr bool kSpecTarget = !std::is_same<Tgt, QuadBowl<NDIM>>::value &&
+                               !std::is_same<Tgt, Linear<NDIM>>::value &&
+                               !std::is_same<Tgt, Const<NDIM>>::value;
+  if constexpr (NDIM <= 6 && kSpecTarget) {
+    if (p.speculate && p.reuse_passes && p.crn && p.mode == kModeSolve && !p.antithetic) {
+      auto launch_spec = [&](auto gs_tag) {
+        constexpr int GS = decltype(gs_tag)::value;
+        constexpr int kPerCta = NT / GS;
+        solve_kernel<Tgt, NDIM, NT, false, false, GS, true>
+            <<<(unsigned)((units + kPerCta - 1) / kPerCta), NT, 0, s>>>(p);
+      };
+      if (p.N <= kWarpUnitMaxN)
+        launch_spec(std::integral_constant<int, 32>{});
+      else if (p.N <= kQuadWarpMaxN)
+        launch_spec(std::integral_constant<int, 128>{});
+      else
+        launch_spec(std::integral_constant<int, kCtaGroup>{});
+      return cudaGetLastError();
+    }
+  }
   if (p.N <= kWarpUnitMaxN)
     launch_group(std::integral_constant<int, 32>{});
   else if (p.N <= kQuadWarpMaxN)

@@ -34,6 +34,7 @@ class SolverConfig:
     sync_check: bool = False
     skip_stationary: bool = False
     reuse_passes: bool = False   # HJMC_FLAG_REUSE_PASSES (exact pass memo under CRN)
+    speculate: bool = False      # HJMC_FLAG_SPECULATE_CLAMPS (memoize the opposite clamp too)
     system: str = "quadratic"
     sys_params: tuple = ()
     target: str = "quad_bowl"
@@ -62,7 +63,8 @@ class SolverConfig:
         c.proposal = _lib.PROPOSALS[self.proposal]
         c.flags = (_lib.FLAG_SYNC_CHECK if self.sync_check else 0) | (
             _lib.FLAG_SKIP_STATIONARY if self.skip_stationary else 0) | (
-            _lib.FLAG_REUSE_PASSES if self.reuse_passes else 0)
+            _lib.FLAG_REUSE_PASSES if self.reuse_passes else 0) | (
+            _lib.FLAG_SPECULATE_CLAMPS if self.speculate else 0)
         return c
 
 

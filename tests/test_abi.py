@@ -82,10 +82,11 @@ def test_create_validation_without_gpu(lib):
     cc.c_min, cc.c_max = 5.0, 1.0
     assert lib.hjmc_create(C.byref(cc), C.byref(h)) == _lib.HJMC_EINVAL
     cc = _lib.Config.from_buffer_copy(c)
-    cc.flags = 8                                   # no such flag bit
+    cc.flags = 16                                  # no such flag bit
     assert lib.hjmc_create(C.byref(cc), C.byref(h)) == _lib.HJMC_EINVAL
     # every declared flag passes validation (then needs a device)
-    cc.flags = _lib.FLAG_SYNC_CHECK | _lib.FLAG_SKIP_STATIONARY | _lib.FLAG_REUSE_PASSES
+    cc.flags = (_lib.FLAG_SYNC_CHECK | _lib.FLAG_SKIP_STATIONARY | _lib.FLAG_REUSE_PASSES |
+                _lib.FLAG_SPECULATE_CLAMPS)
     rcf = lib.hjmc_create(C.byref(cc), C.byref(h))
     assert rcf != _lib.HJMC_EINVAL
     if h.value:

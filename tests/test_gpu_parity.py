@@ -309,15 +309,19 @@ def test_skip_stationary_is_bit_identical():
     assert nocrn.pass_count() == M * 3 * 5
 
 
-@pytest.mark.parametrize("skip,N", [(False, 3000), (True, 3000), (True, 40000), (True, 70000)])
-def test_reuse_passes_is_bit_identical(skip, N):
+@pytest.mark.parametrize("skip,N,spec", [(False, 3000, False), (True, 3000, False),
+                                         (True, 40000, False), (True, 70000, False),
+                                         (True, 3000, True), (False, 40000, True),
+                                         (True, 70000, True)])
+def test_reuse_passes_is_bit_identical(skip, N, spec):
     """HJMC_FLAG_REUSE_PASSES: under CRN a pass is a function of its c, so a pass at a c the
     unit has already used returns the stored sums. Every output equals the full schedule bit
     for bit, and the number of sample passes equals the number of distinct c per (query,
     horizon) trajectory (read off the full run's own chist), stationary skip or not."""
     kw = dict(N=N, K=3, Kp=8)     # N picks the thread group per unit: a warp, 4 warps, the CTA
     base = Solver(SolverConfig.from_preset(I.C2, **kw))
-    memo = Solver(SolverConfig.from_preset(I.C2, reuse_passes=True, skip_stationary=skip, **kw))
+    memo = Solver(SolverConfig.from_preset(I.C2, reuse_passes=True, skip_stationary=skip,
+                                           speculate=spec, **kw))
     x = I.queries(I.C2)[::7]
     a = base.solve_slice(x)
     base.pass_count()
@@ -328,7 +332,10 @@ def test_reuse_passes_is_bit_identical(skip, N):
     ch = a["chist"].cpu().numpy()                     # [K][Kp][M]
     distinct = sum(len(set(ch[j, :, m].tolist())) for j in range(ch.shape[0])
                    for m in range(ch.shape[2]))
-    assert nb == distinct
+    if spec:      # a clamp reached after the opposite clamp was sampled costs no pass
+        assert nb < distinct
+    else:
+        assert nb == distinct
     assert nb < 0.5 * x.shape[0] * 3 * 8               # the C2 slice cycles between the clamps
     # without CRN every pass draws fresh samples: nothing is reused
     nocrn = Solver(SolverConfig.from_preset(I.C2, reuse_passes=True, crn=False, **kw))

@@ -46,7 +46,7 @@ def run(idx, full_slice=False):
     evals = len(ids) * p.N * p.K * p.Kp
     rl = RL.roofline(p.n, p.target)
     # the same subset with the exact shortcuts (bit-identical outputs): stationary skip + memo
-    f = Solver(SolverConfig.from_preset(p, skip_stationary=True, reuse_passes=True))
+    f = Solver(SolverConfig.from_preset(p, skip_stationary=True, reuse_passes=True, speculate=True))
     fout = f.alloc_result(len(ids), hist=False)
     f.solve_slice(x[:warm], qid=qid[:warm])
     torch.cuda.synchronize()

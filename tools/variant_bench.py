@@ -15,7 +15,7 @@ _lib.load("{lib}")
 from paper_2605_18566_b200.solver import Solver, SolverConfig
 p = I.BY_INDEX[{cfg}] if isinstance({cfg}, int) else I.PRESETS[{cfg}]
 kw = {kw}
-skw = {{k: kw.pop(k) for k in ("skip_stationary", "reuse_passes") if k in kw}}
+skw = {{k: kw.pop(k) for k in ("skip_stationary", "reuse_passes", "speculate") if k in kw}}
 p = p.with_(**kw) if kw else p
 s = Solver(SolverConfig.from_preset(p, **skw))
 x = torch.from_numpy(I.queries(p)).cuda()
