@@ -196,7 +196,7 @@ struct SolveSmem {
   float memo_B[kMemo];
   int n_memo;
   float xs[NDIM];   // lane-group kernel: x (+ bτ) staged once; thread 0 derives the pass shift
-  float lg_B;
+  float lg_B, lg_B2;
   double dg[NDIM];  // Dg(x + bτ) for the Laplace proposal (R28)
   float fmax_part[NT / 32];
   double c_next;
@@ -272,10 +272,17 @@ constexpr int kLgLanes = HJMC_LG_LANES;
 constexpr int kLgSpan = 48 / kLgLanes;
 static_assert(kLgLanes == 2 || kLgLanes == 4, "lane groups of 2 or 4");
 
-template <int NDIM, int NT, bool kMaxMode, bool kPursuit = false>
+// Speculative sums of the lane-group pass (HJMC_FLAG_SPECULATE_CLAMPS): the same samples at a
+// second coefficient, weight 2^(A·core + B).
+struct LgSpec {
+  float A, B, S, Mb[kLgSpan];
+};
+
+template <int NDIM, int NT, bool kMaxMode, bool kPursuit = false, bool kSpec = false>
 __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float tau, float sigma_s,
                                         float A, float B, uint32_t w1base, uint32_t qid,
-                                        float& S, float (&Mb)[kLgSpan], float& amax) {
+                                        float& S, float (&Mb)[kLgSpan], float& amax,
+                                        LgSpec* sp = nullptr) {
   constexpr int kBlocks = kLgSpan / 4, kTriples = kLgSpan / 3;
   const int lane = threadIdx.x & 31, l = lane & (kLgLanes - 1);
   const uint32_t slot = (threadIdx.x >> 5) * (32 / kLgLanes) + (lane / kLgLanes);  // sample slot
@@ -340,6 +347,12 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
         S += wt;
 #pragma unroll
         for (int c = 0; c < kLgSpan; ++c) Mb[c] = fmaf(wt, z[c], Mb[c]);
+        if constexpr (kSpec) {
+          const float w2 = ex2_approx(fmaf(sp->A, core, sp->B));
+          sp->S += w2;
+#pragma unroll
+          for (int c = 0; c < kLgSpan; ++c) sp->Mb[c] = fmaf(w2, z[c], sp->Mb[c]);
+        }
       }
     }
   };
@@ -351,7 +364,9 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
 
 // Merge the lane-group sums into sm.sum (double), deterministic order.
 template <int NDIM, int NT>
-__device__ __forceinline__ void lg_reduce(SolveSmem<NDIM, NT>& sm, float S, float (&Mb)[kLgSpan]) {
+__device__ __forceinline__ void lg_reduce(SolveSmem<NDIM, NT>& sm, float S, float (&Mb)[kLgSpan],
+                                          double* dst = nullptr) {
+  double* out = dst ? dst : sm.sum;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, l = lane & (kLgLanes - 1);
 #pragma unroll
   for (int o = kLgLanes; o < 32; o <<= 1) {      // sum over the warp's lane groups
@@ -370,7 +385,7 @@ __device__ __forceinline__ void lg_reduce(SolveSmem<NDIM, NT>& sm, float S, floa
     double acc = 0.0;
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) acc += (double)sm.part[w][col];
-    sm.sum[col] = acc;
+    out[col] = acc;
   }
   __syncthreads();
 }
@@ -494,9 +509,10 @@ __device__ __noinline__ double unit_prologue(const SolveParams& P, const Tgt& tg
 #ifndef HJMC_MINB
 #define HJMC_MINB 0
 #endif
-template <int NDIM, bool kLG>
+template <int NDIM, bool kLG, bool kSpec = false>
 constexpr int min_blocks() {
   if (HJMC_MINB > 0) return HJMC_MINB;
+  if (kLG && kSpec) return kLgLanes == 4 ? 3 : 2;  // + 12 speculative moments per lane
   if (kLG) return kLgLanes == 4 ? 4 : 2;          // 2-lane groups hold 24 + 24 + 16 floats
   return NDIM <= 6 ? 4 : (NDIM <= 16 ? 3 : 1);
 }
@@ -514,7 +530,7 @@ constexpr int min_blocks() {
 // 2-cycle between the clamps costs one sampling pass instead of two.
 template <class Tgt, int NDIM, int NT, bool kLG = false, bool kProp = false, int GS = NT,
           bool kSpec = false>
-__global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(const __grid_constant__ SolveParams P) {
+__global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kernel(const __grid_constant__ SolveParams P) {
   static_assert(GS == NT || (!kLG && GS >= 32 && NT % GS == 0 && GS % 32 == 0),
                 "thread groups smaller than the CTA only for the generic kernel");
   __shared__ SolveSmem<NDIM, GS> smv[NT / GS];
@@ -654,8 +670,30 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG>()) solve_kernel(cons
     if (hit < 0) {
       if constexpr (kLG) {
         float S, Mb[kLgSpan], amax;
-        lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax);
-        lg_reduce<NDIM, NT>(sm, S, Mb);
+        bool plain_lg = true;
+        if constexpr (kSpec) {
+          if (do_spec) {
+            LgSpec sp;
+            sp.A = opaque((float)(-c_spec * kLog2e));
+            if (tid == 0) sm.lg_B2 = -sp.A * tgt.core_lower(sm.xs, sigma);  // as a pass at c_spec
+            __syncthreads();
+            sp.B = opaque(sm.lg_B2);
+            sp.S = 0.f;
+#pragma unroll
+            for (int c2 = 0; c2 < kLgSpan; ++c2) sp.Mb[c2] = 0.f;
+            lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit, true>(
+                P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax, &sp);
+            lg_reduce<NDIM, NT>(sm, S, Mb);
+            lg_reduce<NDIM, NT>(sm, sp.S, sp.Mb, sm.sum2);
+            B_spec = sp.B;
+            plain_lg = false;
+          }
+        }
+        if (plain_lg) {
+          lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A,
+                                                                       B, w1base, id, S, Mb, amax);
+          lg_reduce<NDIM, NT>(sm, S, Mb);
+        }
       } else {
         float S, Mz[NDIM];
         bool plain = true;
@@ -783,7 +821,10 @@ cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
   if (units > 0x7FFFFFFFLL) return cudaErrorInvalidValue;
   if constexpr (UseLaneGroups<Tgt, NDIM>::value) {
     if (!p.antithetic && !p.proposal) {
-      solve_kernel<Tgt, NDIM, NT, true, false><<<(unsigned)units, NT, 0, s>>>(p);
+      if (p.speculate && p.reuse_passes && p.crn && p.mode == kModeSolve)
+        solve_kernel<Tgt, NDIM, NT, true, false, NT, true><<<(unsigned)units, NT, 0, s>>>(p);
+      else
+        solve_kernel<Tgt, NDIM, NT, true, false><<<(unsigned)units, NT, 0, s>>>(p);
       return cudaGetLastError();
     }
   }

@@ -347,12 +347,15 @@ def test_reuse_passes_lane_groups_and_proposal():
     """The memo is shared by the lane-group kernel (n = 45 pair union) and the Laplace
     proposal (the centre μ follows from c): outputs bit-identical to the full schedule."""
     for preset, extra in ((I.C5.with_(N=2048, K=2, Kp=4, grid_pts=8), {}),
+                          (I.C5.with_(N=2048, K=2, Kp=6, grid_pts=8), {"speculate": True}),
+                          (I.C4.with_(N=3000, K=2, Kp=6, grid_pts=9), {"speculate": True}),
                           (I.C2.with_(N=2048, K=2, Kp=6, grid_pts=11), {"proposal": "laplace"}),
                           (I.C2.with_(N=5001, K=2, Kp=6, grid_pts=11), {"antithetic": True}),
                           (I.C3.with_(N=2048, K=2, Kp=5, grid_pts=9), {})):
         x = I.queries(preset)
         base = Solver(SolverConfig.from_preset(preset, **extra))
-        memo = Solver(SolverConfig.from_preset(preset, reuse_passes=True, **extra))
+        memo = Solver(SolverConfig.from_preset(preset, reuse_passes=True, skip_stationary=True,
+                                               **extra))
         a = base.solve_slice(x)
         b = memo.solve_slice(x)
         for k in a:

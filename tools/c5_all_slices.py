@@ -1,5 +1,6 @@
 """BASELINE config 5 as a whole on one B200: all 8 slices (θ₁ = kπ/4) of 256² queries, each with
-the exact shortcuts (stationary skip + pass memo; bit-identical to the full schedule), and the
+the exact shortcuts (stationary skip + pass memo + speculative clamps; bit-identical to the full
+schedule), and the
 full schedule on two of them — the 1-GPU point of the 1/2/4/8-GPU query-sharded run (one slice
 per GPU at 8 GPUs). Usage: python tools/c5_all_slices.py [--full 0,4]"""
 import json
@@ -28,11 +29,13 @@ def timed(solver, x, qid):
 
 
 if __name__ == "__main__":
-    full = [int(a) for a in sys.argv[sys.argv.index("--full") + 1].split(",")] if "--full" in sys.argv else [0, 4]
+    full = ([int(a) for a in sys.argv[sys.argv.index("--full") + 1].split(",") if a]
+            if "--full" in sys.argv else [0, 4])
     p = I.C5
     per = p.grid_pts * p.grid_pts
     x_all = torch.from_numpy(I.queries(p)).cuda()
-    fast = Solver(SolverConfig.from_preset(p, skip_stationary=True, reuse_passes=True))
+    fast = Solver(SolverConfig.from_preset(p, skip_stationary=True, reuse_passes=True,
+                                           speculate=True))
     base = Solver(SolverConfig.from_preset(p))
     fast.solve_slice(x_all[:296])                               # warm both kernels
     base.solve_slice(x_all[:296])
