@@ -514,6 +514,7 @@ constexpr int min_blocks() {
   if (HJMC_MINB > 0) return HJMC_MINB;
   if (kLG && kSpec) return kLgLanes == 4 ? 3 : 2;  // + 12 speculative moments per lane
   if (kLG) return kLgLanes == 4 ? 4 : 2;          // 2-lane groups hold 24 + 24 + 16 floats
+  if (kSpec && NDIM > 6) return 2;                 // + n + 1 speculative sums (n ≤ 16)
   return NDIM <= 6 ? 4 : (NDIM <= 16 ? 3 : 1);
 }
 
@@ -846,7 +847,7 @@ cudaError_t launch_solve(const SolveParams& p, int64_t units, cudaStream_t s) {
   constexpr bool kSpecTarget = !std::is_same<Tgt, QuadBowl<NDIM>>::value &&
                                !std::is_same<Tgt, Linear<NDIM>>::value &&
                                !std::is_same<Tgt, Const<NDIM>>::value;
-  if constexpr (NDIM <= 6 && kSpecTarget) {
+  if constexpr (NDIM <= 16 && kSpecTarget) {
     if (p.speculate && p.reuse_passes && p.crn && p.mode == kModeSolve && !p.antithetic) {
       auto launch_spec = [&](auto gs_tag) {
         constexpr int GS = decltype(gs_tag)::value;
