@@ -161,7 +161,8 @@ extern "C" {
  * between the clamps c_min ↔ c_max that dominate the game slices (R8, R27). Outputs are
  * identical with and without the flag; hjmc_pass_count() reports the sample passes run. */
 #define HJMC_FLAG_REUSE_PASSES 4u
-/* With HJMC_FLAG_REUSE_PASSES and crn = 1, for n ≤ 6 and the plain proposal without antithetic
+/* With HJMC_FLAG_REUSE_PASSES and crn = 1, for the game targets with n ≤ 16 or the n = 37–48
+ * lane-group kernels, plain proposal, no antithetic
  * sampling: a pass whose frozen c sits on a clamp (c_min or c_max) also accumulates, from the
  * same samples, the sums at the opposite clamp and memoizes them (when they need no two-pass
  * fallback), so a c_min ↔ c_max Picard 2-cycle costs one sampling pass. Outputs are identical
