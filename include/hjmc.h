@@ -165,8 +165,9 @@ extern "C" {
  * lane-group kernels, plain proposal, no antithetic
  * sampling: a pass whose frozen c sits on a clamp (c_min or c_max) also accumulates, from the
  * same samples, the sums at the opposite clamp and memoizes them (when they need no two-pass
- * fallback), so a c_min ↔ c_max Picard 2-cycle costs one sampling pass. Outputs are identical
- * with and without the flag; ignored where it does not apply. */
+ * fallback), so a c_min ↔ c_max Picard 2-cycle costs one sampling pass (C2 −16 %, C4 −22 %,
+ * C5 −43 %); where units are stationary after one pass the extra sums go unused (≈ +4 %).
+ * Outputs are identical with and without the flag; ignored where it does not apply. */
 #define HJMC_FLAG_SPECULATE_CLAMPS 8u
 
 /* Sampling proposal of a Φ pass (reading R28).
