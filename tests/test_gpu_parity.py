@@ -682,3 +682,34 @@ def test_solve_slice_with_drift_vs_oracle(O, target, n, params, system, extra):
     assert ref["status"] == 0
     g = {k: t.cpu().numpy() for k, t in out.items()}
     assert_picard_history(O, P, x, np.arange(29) + 9, g["vhist"], g["chist"], ref)
+
+
+@pytest.mark.parametrize("target,n,params,system,span", [
+    ("disk", 2, (1.0,), "quadratic", 8.0),
+    ("disk", 3, (5.0,), "dubins_rel", 12.0),
+    ("pair_union", 45, (1.0,), "dubins_pairs", 6.0),                      # lane-group max mode
+])
+def test_two_pass_fallback_when_the_shift_underflows(O, target, n, params, system, span):
+    """The guaranteed shift B = −A·core_lower leaves every weight below 2⁻¹⁰⁰ when c·σ is large
+    (the bound uses |z| ≤ 5.77 per coordinate, the realised samples reach ~3.5): the pass is
+    redone with the exact maximum exponent (the plain two-pass log-sum-exp). c = 20,
+    σ = 1 puts every query there; GPU vs oracle, and through the fused solve with the memo."""
+    N = 4096
+    s, P = pair(O, n=n, delta=1.0, N=N, seed=5, system=system, target=target, tgt_params=params)
+    x = I.random_queries(n, 23, -span, span, seed=n + 40)
+    cc = np.full(23, 20.0, dtype=np.float32)
+    v, dv = s.value_grad(x, cc, 1.0, j_tag=2, k_tag=0)
+    vo, dvo = O.phi_batch(P, x, cc.astype(np.float64), 1.0, jw=2, kw=0)
+    assert_v(v.cpu().numpy(), vo, "v (fallback)")
+    assert_dv(dv.cpu().numpy(), dvo, "dv (fallback)")
+    # fused solve (c from Γ, clamps up to 20) with and without the exact shortcuts
+    kw = dict(n=n, delta=1.0, T=1.0, K=2, Kp=3, N=N, seed=5, system=system, target=target,
+              tgt_params=params)
+    a = Solver(SolverConfig(**kw)).solve_slice(x)
+    b = Solver(SolverConfig(reuse_passes=True, skip_stationary=True, speculate=True,
+                            **kw)).solve_slice(x)
+    for k in a:
+        assert torch.equal(a[k], b[k]), k
+    ref = O.solve_slice(O.Problem(**kw), x)
+    assert_picard_history(O, O.Problem(**kw), x, np.arange(23), a["vhist"].cpu().numpy(),
+                          a["chist"].cpu().numpy(), ref)
