@@ -56,7 +56,8 @@ def test_random_value_grad_parity(oracle_mod, i, case):
     s = Solver(SolverConfig(**kw))
     P = O.Problem(**kw)
     x = I.random_queries(case["n"], case["M"], -case["span"], case["span"], seed=i)
-    cc = np.full(case["M"], case["c"], dtype=np.float32)
+    # per-query coefficients around the case's c (the pass freezes c per query, R5)
+    cc = (case["c"] * np.exp(np.random.default_rng(i).uniform(-1, 1, case["M"]))).astype(np.float32)
     v, dv = s.value_grad(x, cc, case["tau"], j_tag=i + 1, k_tag=i % 7, qid_base=case["qid_base"])
     vo, dvo = O.phi_batch(P, x, cc.astype(np.float64), case["tau"], qid_base=case["qid_base"],
                           jw=i + 1, kw=i % 7)
