@@ -76,7 +76,7 @@ int main(void) {
   memset(&hres, 0, sizeof(hres));
   hres.v = v2;
   hres.tube = t2;
-  CHECK(hjmc_solve_slice_host(h, x, 0, M, NULL, &hres));
+  CHECK(hjmc_solve_slice_host(h, x, NULL, 0, M, NULL, &hres));
 
   int same = memcmp(v1, v2, sizeof(float) * M) == 0 && memcmp(t1, t2, sizeof(float) * M) == 0;
   int inside = 0;
@@ -100,7 +100,7 @@ int main(void) {
   cudaMalloc((void**)&piters, sizeof(int32_t) * K);
   cudaMalloc((void**)&peps, sizeof(double) * K * Kp);
   cudaMalloc((void**)&pdsup, sizeof(double) * K * Kp);
-  CHECK(hjmc_picard_solve(h, dx, NULL, 0, M, NULL, 0.0, Kp, pv, NULL, pc, piters, peps, pdsup,
+  CHECK(hjmc_picard_solve(h, dx, NULL, 0, M, NULL, 0.0, Kp, pv, NULL, pc, piters, peps, pdsup, NULL,
                           NULL));
   cudaDeviceSynchronize();
   float* v3 = (float*)malloc(sizeof(float) * M);

@@ -133,7 +133,7 @@ extern "C" {
 #endif
 
 #define HJMC_VERSION_MAJOR 0
-#define HJMC_VERSION_MINOR 1
+#define HJMC_VERSION_MINOR 2
 
 /* Error codes (S:540 maps config errors to exit 2 and numeric errors to exit 3). */
 #define HJMC_OK 0
@@ -286,11 +286,13 @@ HJMC_API int hjmc_value_grad(hjmc_handle* h, const float* x, const float* c, con
 HJMC_API int hjmc_solve_slice(hjmc_handle* h, const float* x, const uint32_t* qid, uint32_t qid_base,
                      int64_t M, const float* drift, const hjmc_result* out, void* stream);
 
-/* End-to-end convenience: the same solve with HOST buffers. Copies x (and drift) to handle-owned
- * device scratch, solves, copies the requested outputs back to the HOST pointers in *out_host,
- * and synchronises. Returns HJMC_ENUMERIC on a numerical failure. */
-HJMC_API int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, uint32_t qid_base, int64_t M,
-                          const float* drift_host, const hjmc_result* out_host);
+/* End-to-end convenience: the same solve with HOST buffers. Copies x (and qid, drift) to
+ * handle-owned device scratch, solves, copies the requested outputs back to the HOST pointers in
+ * *out_host, and synchronises. qid_host [M] (may be NULL → qid_base + m) gives explicit global
+ * query ids, as in hjmc_solve_slice. Returns HJMC_ENUMERIC on a numerical failure. */
+HJMC_API int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, const uint32_t* qid_host,
+                          uint32_t qid_base, int64_t M, const float* drift_host,
+                          const hjmc_result* out_host);
 
 /* ---- Stepwise Picard: Algorithm 1 with its convergence test (step 5) ------------
  * The fused solve runs a fixed Kp. Algorithm 1 instead stops when
@@ -313,6 +315,31 @@ HJMC_API int hjmc_picard_begin(hjmc_handle* h, const float* x, const uint32_t* q
 HJMC_API int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, float* v,
                               float* dv, float* c, double* partials, void* stream);
 
+/* Algorithm 1's stopping test (step 5) on residual partials that the caller has already
+ * combined across shards (HOST partials [K][3]: Σ(v^(k+1)−v^(k))², Σ(v^(k))² summed, max
+ * |v^(k+1)−v^(k)| maxed — one all-reduce): for every horizon j with active[j] != 0,
+ *   ε_j = sqrt(Σ(v^(k+1)−v^(k))² / max(Σ(v^(k))², 1e-300))   (relative L2, R11)
+ * is written to eps[j] and the sup-norm difference to dsup[j] (Theorem 2's d_k, P:346–360;
+ * NaN for inactive horizons; either may be NULL), and horizon j is retired (active[j] = 0)
+ * when ε_j < tol. *n_active (may be NULL) receives the horizons still active. The same double
+ * expression as the decision kernel of hjmc_picard_solve, so a host-driven (e.g. sharded) loop
+ * takes identical decisions. Host-only, no handle; EINVAL for K < 1, tol < 0 or NULL
+ * partials / active. */
+HJMC_API int hjmc_picard_decide(const double* partials, int32_t K, double tol, uint8_t* active,
+                                double* eps, double* dsup, int32_t* n_active);
+
+/* Post-hoc residuals (a12; R11) from summed partials (HOST [count][2] = (num, den), e.g.
+ * hjmc_residual_partials all-reduced over shards): eps[i] = sqrt(num / max(den, 1e-300)). */
+HJMC_API int hjmc_residual_eps(const double* partials, int64_t count, double* eps);
+
+/* The running-min reach tube of per-horizon final iterates, with the BRAT clamp when
+ * hjmc_set_avoid installed an obstacle:
+ *   tube[m] = max( min( g(x_m), min_j vfinal[j][m] ), ℓ(x_m) )
+ * x [M][n], vfinal [K][M] (e.g. the v output of hjmc_picard_pass / hjmc_picard_solve), tube [M]:
+ * device pointers, stream-ordered. g(x) goes through handle scratch. */
+HJMC_API int hjmc_tube(hjmc_handle* h, const float* x, int64_t M, const float* vfinal, float* tube,
+                       void* stream);
+
 /* Algorithm 1 with its stopping test (iterate until ε_j(k) < tol, step 5), for every
  * horizon, entirely on the device: hjmc_picard_begin, then one CUDA graph whose conditional
  * 'while' node repeats {Φ pass of the still-active horizons, residual partials, decision} —
@@ -321,7 +348,9 @@ HJMC_API int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, 
  * retires horizon j when ε_j(k) < tol, and stops the loop when none is left or after max_iter
  * passes. Outputs (device): v [K][M], dv [K][M][n] (may be NULL), c [K][M] (may be NULL) of each
  * horizon's final iterate; iters [K] (int32) passes run per horizon; eps, dsup [K][max_iter]
- * (double) ε_j(k) and max_m |v^(k+1) − v^(k)|, NaN past the stop. Same kernels, counters and
+ * (double) ε_j(k) and max_m |v^(k+1) − v^(k)|, NaN past the stop; tube [M] (may be NULL) the
+ * running-min tube over the horizons' final iterates with the BRAT clamp, exactly hjmc_tube's
+ * (P:194–210), formed inside the same graph after the loop. Same kernels, counters and
  * reduction order as hjmc_picard_pass driven from the host: identical results. Stream-ordered
  * (asynchronous): one graph launch on stream; the instantiated graph is cached in the handle and
  * reused while the arguments and the handle's dynamics / target / avoid set are unchanged.
@@ -330,7 +359,7 @@ HJMC_API int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, 
 HJMC_API int hjmc_picard_solve(hjmc_handle* h, const float* x, const uint32_t* qid,
                                uint32_t qid_base, int64_t M, const float* drift, double tol,
                                int32_t max_iter, float* v, float* dv, float* c, int32_t* iters,
-                               double* eps, double* dsup, void* stream);
+                               double* eps, double* dsup, float* tube, void* stream);
 
 /* g(x) and the analytic Dg(x) used for c^(0) (dev pointers; dg may be NULL). */
 HJMC_API int hjmc_eval_target(hjmc_handle* h, const float* x, int64_t M, float* g, float* dg,

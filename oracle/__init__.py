@@ -77,6 +77,11 @@ def lib():
         L.orc_picard_adaptive.argtypes = [pp, fp, up, C.c_uint32, C.c_int64, C.c_double, C.c_int32,
                                           dp, dp, dp, dp, C.c_int32]
         L.orc_picard_adaptive.restype = C.c_int
+        L.orc_phi_batch.argtypes = [pp, fp, C.POINTER(C.c_int64), up, dp, dp, up, up, C.c_int64,
+                                    dp, dp, C.c_int32]
+        L.orc_phi_batch.restype = C.c_int
+        L.orc_tube.argtypes = [pp, fp, C.c_int64, dp, dp]
+        L.orc_tube.restype = None
         L.orc_max_threads.restype = C.c_int
         _lib = L
     return _lib
@@ -228,6 +233,28 @@ def phi_batch(P: Problem, x, c, tau: float, qid_base: int = 0, jw: int = 1, kw: 
     return v, dv
 
 
+def phi_items(P: Problem, x, xi, qid, c, tau, jw, kw, nthreads: int = 0, want_dv: bool = True):
+    """Φ at independent items i: query x[xi[i]] (the fp32 array, converted to double), global
+    id qid[i], frozen coefficient c[i], time-to-go tau[i], counter tags jw[i], kw[i] — a plain
+    OpenMP loop of orc_phi (orc_phi_batch). Returns (v[count], dv[count][n] or None)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    cnt = len(xi)
+    arr = lambda a, dt: np.ascontiguousarray(np.broadcast_to(np.asarray(a), (cnt,)), dtype=dt)
+    xi_, q_ = arr(xi, np.int64), arr(qid, np.uint32)
+    c_, t_ = arr(c, np.float64), arr(tau, np.float64)
+    j_, k_ = arr(jw, np.uint32), arr(kw, np.uint32)
+    v = np.zeros(cnt)
+    dv = np.zeros((cnt, P.n)) if want_dv else None
+    up = C.POINTER(C.c_uint32)
+    st = lib().orc_phi_batch(C.byref(P.struct()), x.ctypes.data_as(C.POINTER(C.c_float)),
+                             xi_.ctypes.data_as(C.POINTER(C.c_int64)), q_.ctypes.data_as(up),
+                             _dp(c_), _dp(t_), j_.ctypes.data_as(up), k_.ctypes.data_as(up), cnt,
+                             _dp(v), _dp(dv), nthreads)
+    if st == 1:
+        raise MemoryError("oracle phi: allocation failed")
+    return v, dv
+
+
 def solve_slice(P: Problem, x, drift=None, qid_base: int = 0, qids=None, nthreads: int = 0):
     """Algorithm 1 over all horizons for the fp32 queries x[M][n]; returns a dict of float64."""
     x = np.ascontiguousarray(x, dtype=np.float32)
@@ -253,7 +280,8 @@ def solve_slice(P: Problem, x, drift=None, qid_base: int = 0, qids=None, nthread
 def picard_adaptive(P: Problem, x, tol: float, max_iter: int, qid_base: int = 0, qids=None,
                     nthreads: int = 0):
     """Algorithm 1 with the convergence test, per horizon. Returns v [K][M], iters [K],
-    eps [K][max_iter], d_sup [K][max_iter]."""
+    eps [K][max_iter], d_sup [K][max_iter], tube [M] (orc_tube: running min with the BRAT
+    clamp)."""
     x = np.ascontiguousarray(x, dtype=np.float32)
     M, K = x.shape[0], P.K
     v = np.zeros((K, M))
@@ -265,7 +293,10 @@ def picard_adaptive(P: Problem, x, tol: float, max_iter: int, qid_base: int = 0,
                                    q.ctypes.data_as(C.POINTER(C.c_uint32)) if q is not None else None,
                                    qid_base, M, tol, max_iter, _dp(v), _dp(iters), _dp(eps),
                                    _dp(dsup), nthreads)
-    return {"v": v, "iters": iters.astype(int), "eps": eps, "d_sup": dsup, "status": st}
+    tube = np.zeros(M)
+    lib().orc_tube(C.byref(P.struct()), x.ctypes.data_as(C.POINTER(C.c_float)), M, _dp(v), _dp(tube))
+    return {"v": v, "iters": iters.astype(int), "eps": eps, "d_sup": dsup, "tube": tube,
+            "status": st}
 
 
 def gamma_sensitivity(P: Problem, x, p, rel: float = 1e-6) -> float:

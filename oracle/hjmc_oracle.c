@@ -408,6 +408,35 @@ int orc_phi(const orc_problem* P, const double* x, const double* drift, uint32_t
   return ok ? 0 : 2;
 }
 
+/* Phi at a list of independent items (one per (query, horizon, frozen c)): item i evaluates
+ * orc_phi at x[xi[i]] with global id qid[i], coefficient c[i], time-to-go tau[i] and counter
+ * tags (jw[i], kw[i]); outputs v[i] and dv[i][n] (dv may be NULL). A plain loop over orc_phi
+ * (OpenMP over items) — the teacher-forced parity tests use it to evaluate Phi at the oracle's
+ * own coefficient history. Returns the last nonzero orc_phi status, else 0. */
+int orc_phi_batch(const orc_problem* P, const float* x, const int64_t* xi, const uint32_t* qid,
+                  const double* c, const double* tau, const uint32_t* jw, const uint32_t* kw,
+                  int64_t count, double* v, double* dv, int32_t nthreads) {
+  int status = 0;
+  const int n = P->n;
+#ifdef _OPENMP
+  const int nt = nthreads > 0 ? nthreads : omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+#endif
+  for (int64_t i = 0; i < count; ++i) {
+    double xm[ORC_MAX_N];
+    for (int d = 0; d < n; ++d) xm[d] = (double)x[xi[i] * n + d];
+    int st = orc_phi(P, xm, NULL, qid[i], c[i], tau[i], jw[i], kw[i], &v[i],
+                     dv ? dv + (size_t)i * (size_t)n : NULL, NULL, NULL);
+    if (st) {
+#ifdef _OPENMP
+#pragma omp atomic write
+#endif
+      status = st;
+    }
+  }
+  return status;
+}
+
 /* ------------------------------------------------------------------------------------------
  * Algorithm 1 per query and horizon, then the running-min tube (R9).
  *   tau_j = j T / K (R9); v^(0) = g; c^(0) = Gamma(x, Dg);
@@ -550,6 +579,25 @@ int orc_picard_adaptive(const orc_problem* P, const float* x, const uint32_t* qi
   }
   free(vprev); free(vcur); free(c);
   return status;
+}
+
+/* Running-min reach tube of per-horizon final iterates with the BRAT clamp (
+ * S:345): tube[m] = max( min( g(x_m), min_j vfinal[j][m] ), l(x_m) ), l = -inf
+ * without an obstacle. x is the fp32 query array (converted to double), vfinal [K][M]. */
+void orc_tube(const orc_problem* P, const float* x, int64_t M, const double* vfinal, double* tube) {
+  int n = P->n, K = P->K;
+  for (int64_t m = 0; m < M; ++m) {
+    double xm[ORC_MAX_N];
+    for (int d = 0; d < n; ++d) xm[d] = (double)x[m * n + d];
+    double t = orc_target_g(P, xm);
+    for (int j = 0; j < K; ++j) {
+      double vj = vfinal[(size_t)j * (size_t)M + (size_t)m];
+      if (vj < t) t = vj;
+    }
+    double l = orc_avoid_l(P, xm);
+    if (l > t) t = l;
+    tube[m] = t;
+  }
 }
 
 /* Picard residual partial sums (relative L2 over the slice, R11), v^(0) = g. */

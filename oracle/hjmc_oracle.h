@@ -14,9 +14,11 @@
  *   orc_gamma           pinned: quadratic c = 1/δ_eff, clamp/floor cases
  *   orc_phi             pinned: constant/linear/quadratic closed forms, Gauss–Hermite and
  *                       noncentral-χ² quadrature, Jensen bounds, shift/translation identities
+ *   orc_phi_batch       a plain OpenMP loop of orc_phi over independent items
  *   orc_solve_slice     pinned: quadratic CRN stationarity, tube ≤ g and ≤ every v_j,
  *                       per-sample BRT band bound; every step is orc_phi + orc_gamma; the MC
  *                       Picard reproduces a Gauss–Hermite-quadrature Picard on clamped queries
+ *   orc_tube            pinned: tube ≤ g, ≤ every v_j, = max(·, ℓ) with an obstacle (same as solve_slice's)
  *   orc_avoid_l         pinned: BRAT clamp identities (disk obstacle)
  *   orc_picard_adaptive pinned: equals the fixed schedule at tol = 0, stops at the first
  *                       ε < tol (Algorithm 1 step 5); SPEC's contraction example
@@ -82,12 +84,16 @@ double orc_gamma(const orc_problem* P, const double* x, const double* p);
 int orc_phi(const orc_problem* P, const double* x, const double* drift, uint32_t qid, double c,
             double tau, uint32_t jw, uint32_t kw, double* v, double* dv, double* diag,
             double* se_dv);
+int orc_phi_batch(const orc_problem* P, const float* x, const int64_t* xi, const uint32_t* qid,
+                  const double* c, const double* tau, const uint32_t* jw, const uint32_t* kw,
+                  int64_t count, double* v, double* dv, int32_t nthreads);
 int orc_solve_slice(const orc_problem* P, const float* x, const float* drift, const uint32_t* qid,
                     uint32_t qid_base, int64_t M, double* v, double* dv, double* c, double* tube,
                     double* vhist, double* chist, double* g0, double* dvhist, int32_t nthreads);
 int orc_picard_adaptive(const orc_problem* P, const float* x, const uint32_t* qid,
                         uint32_t qid_base, int64_t M, double tol, int32_t max_iter, double* v_out,
                         double* iters, double* eps, double* dsup, int32_t nthreads);
+void orc_tube(const orc_problem* P, const float* x, int64_t M, const double* vfinal, double* tube);
 void orc_residual_partials(const double* vhist, const double* g0, int32_t K, int32_t Kp,
                            int64_t M, double* out);
 int orc_max_threads(void);

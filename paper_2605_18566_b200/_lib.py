@@ -31,7 +31,7 @@ EXPORTS = [
     "hjmc_eval_target", "hjmc_eval_hamiltonian", "hjmc_debug_normals", "hjmc_check",
     "hjmc_last_bad_query", "hjmc_last_error", "hjmc_residual_partials", "hjmc_version",
     "hjmc_pass_count", "hjmc_picard_begin", "hjmc_picard_pass", "hjmc_picard_solve",
-    "hjmc_set_avoid",
+    "hjmc_set_avoid", "hjmc_picard_decide", "hjmc_residual_eps", "hjmc_tube",
 ]
 
 
@@ -79,7 +79,7 @@ def load(path: str = LIB_PATH):
     L.hjmc_supported.argtypes = [C.c_int32, C.c_int32]
     L.hjmc_value_grad.argtypes = [vp, vp, vp, vp, u32, i64, fp, u32, u32, vp, vp, vp, vp]
     L.hjmc_solve_slice.argtypes = [vp, vp, vp, u32, i64, vp, C.POINTER(Result), vp]
-    L.hjmc_solve_slice_host.argtypes = [vp, vp, u32, i64, vp, C.POINTER(Result)]
+    L.hjmc_solve_slice_host.argtypes = [vp, vp, vp, u32, i64, vp, C.POINTER(Result)]
     L.hjmc_eval_target.argtypes = [vp, vp, i64, vp, vp, vp]
     L.hjmc_eval_hamiltonian.argtypes = [vp, vp, vp, i64, vp, vp, vp]
     L.hjmc_debug_normals.argtypes = [vp, u32, u32, u32, u32, u32, vp, vp, vp]
@@ -95,7 +95,10 @@ def load(path: str = LIB_PATH):
     L.hjmc_picard_begin.argtypes = [vp, vp, vp, u32, i64, vp, vp]
     L.hjmc_picard_pass.argtypes = [vp, C.c_int32, vp, vp, vp, vp, vp, vp]
     L.hjmc_picard_solve.argtypes = [vp, vp, vp, u32, i64, vp, C.c_double, C.c_int32, vp, vp, vp,
-                                    vp, vp, vp, vp]
+                                    vp, vp, vp, vp, vp]
+    L.hjmc_picard_decide.argtypes = [vp, C.c_int32, C.c_double, vp, vp, vp, vp]
+    L.hjmc_residual_eps.argtypes = [vp, i64, vp]
+    L.hjmc_tube.argtypes = [vp, vp, i64, vp, vp, vp]
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"libhjmc.so lacks {name}")

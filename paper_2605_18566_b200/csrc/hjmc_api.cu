@@ -11,10 +11,21 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/hjmc.h"
 #include "hjmc_kernels.cuh"
 
 using namespace hjmc;
+
+namespace {
+// NVTX range over one C-ABI call (header-only NVTX v3: a no-op unless a profiler injects it), so
+// nsys / ncu --nvtx timelines attribute kernels to the library entry point that launched them.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 struct hjmc_handle {
   hjmc_config cfg{};
@@ -349,6 +360,7 @@ int hjmc_set_target(hjmc_handle* h, int32_t id, const float* params, int32_t np)
 int hjmc_value_grad(hjmc_handle* h, const float* x, const float* c, const uint32_t* qid,
                     uint32_t qid_base, int64_t M, float tau, uint32_t j_tag, uint32_t k_tag,
                     const float* drift, float* v, float* dv, void* stream) {
+  NvtxRange nvtx_range("hjmc_value_grad");
   int rc = ready(h);
   if (rc) return rc;
   if (M < 0) return fail(h, HJMC_EINVAL, "M < 0");
@@ -383,6 +395,7 @@ int hjmc_value_grad(hjmc_handle* h, const float* x, const float* c, const uint32
 
 int hjmc_solve_slice(hjmc_handle* h, const float* x, const uint32_t* qid, uint32_t qid_base,
                      int64_t M, const float* drift, const hjmc_result* out, void* stream) {
+  NvtxRange nvtx_range("hjmc_solve_slice");
   int rc = ready(h);
   if (rc) return rc;
   if (M < 0) return fail(h, HJMC_EINVAL, "M < 0");
@@ -431,8 +444,10 @@ int hjmc_solve_slice(hjmc_handle* h, const float* x, const uint32_t* qid, uint32
   return sync_check_if_requested(h, s);
 }
 
-int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, uint32_t qid_base, int64_t M,
-                          const float* drift_host, const hjmc_result* out_host) {
+int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, const uint32_t* qid_host,
+                          uint32_t qid_base, int64_t M, const float* drift_host,
+                          const hjmc_result* out_host) {
+  NvtxRange nvtx_range("hjmc_solve_slice_host");
   int rc = ready(h);
   if (rc) return rc;
   if (M < 0) return fail(h, HJMC_EINVAL, "M < 0");
@@ -440,13 +455,13 @@ int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, uint32_t qid_base
   if (!x_host || !out_host) return fail(h, HJMC_EINVAL, "x_host and out_host are required");
   if ((rc = set_device(h))) return rc;
   const size_t n = (size_t)h->cfg.n, K = (size_t)h->cfg.K, Kp = (size_t)h->cfg.Kp, m = (size_t)M;
-  // staging layout: x | drift | v | dv | c | tube | vhist | chist | g0
-  const size_t sizes[9] = {m * n, drift_host ? m * n : 0, out_host->v ? m : 0,
-                           out_host->dv ? m * n : 0, out_host->c ? m : 0, out_host->tube ? m : 0,
-                           out_host->vhist ? K * Kp * m : 0, out_host->chist ? K * Kp * m : 0,
-                           out_host->g0 ? m : 0};
-  size_t total = 0, off[9];
-  for (int i = 0; i < 9; ++i) {
+  // staging layout (4-byte words): x | drift | v | dv | c | tube | vhist | chist | g0 | qid
+  const size_t sizes[10] = {m * n, drift_host ? m * n : 0, out_host->v ? m : 0,
+                            out_host->dv ? m * n : 0, out_host->c ? m : 0, out_host->tube ? m : 0,
+                            out_host->vhist ? K * Kp * m : 0, out_host->chist ? K * Kp * m : 0,
+                            out_host->g0 ? m : 0, qid_host ? m : 0};
+  size_t total = 0, off[10];
+  for (int i = 0; i < 10; ++i) {
     off[i] = total;
     total += (sizes[i] + 63) & ~size_t(63);  // 256-byte aligned sub-buffers
   }
@@ -457,11 +472,14 @@ int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, uint32_t qid_base
                                   cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess && drift_host)
     e = cudaMemcpyAsync(base + off[1], drift_host, sizes[1] * sizeof(float), cudaMemcpyHostToDevice, s);
+  uint32_t* dqid = qid_host ? reinterpret_cast<uint32_t*>(base + off[9]) : nullptr;
+  if (e == cudaSuccess && qid_host)
+    e = cudaMemcpyAsync(dqid, qid_host, sizes[9] * sizeof(uint32_t), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(h, e, "H2D copy");
   hjmc_result dres{};
   float** dptr[7] = {&dres.v, &dres.dv, &dres.c, &dres.tube, &dres.vhist, &dres.chist, &dres.g0};
   for (int i = 0; i < 7; ++i) *dptr[i] = sizes[2 + i] ? base + off[2 + i] : nullptr;
-  rc = hjmc_solve_slice(h, base + off[0], nullptr, qid_base, M, drift_host ? base + off[1] : nullptr,
+  rc = hjmc_solve_slice(h, base + off[0], dqid, qid_base, M, drift_host ? base + off[1] : nullptr,
                         &dres, (void*)s);
   if (rc) return rc;
   float* hptr[7] = {out_host->v, out_host->dv, out_host->c, out_host->tube, out_host->vhist,
@@ -477,6 +495,7 @@ int hjmc_solve_slice_host(hjmc_handle* h, const float* x_host, uint32_t qid_base
 
 int hjmc_picard_begin(hjmc_handle* h, const float* x, const uint32_t* qid, uint32_t qid_base,
                       int64_t M, const float* drift, void* stream) {
+  NvtxRange nvtx_range("hjmc_picard_begin");
   int rc = ready(h);
   if (rc) return rc;
   if (M < 1 || !x) return fail(h, HJMC_EINVAL, "need M >= 1 and x");
@@ -525,8 +544,9 @@ int hjmc_picard_begin(hjmc_handle* h, const float* x, const uint32_t* qid, uint3
 // handle and relaunched while the arguments and the problem are unchanged.
 int hjmc_picard_solve(hjmc_handle* h, const float* x, const uint32_t* qid, uint32_t qid_base,
                       int64_t M, const float* drift, double tol, int32_t max_iter, float* v,
-                      float* dv, float* c, int32_t* iters, double* eps, double* dsup,
+                      float* dv, float* c, int32_t* iters, double* eps, double* dsup, float* tube,
                       void* stream) {
+  NvtxRange nvtx_range("hjmc_picard_solve");
   int rc = ready(h);
   if (rc) return rc;
   if (M < 1 || !x) return fail(h, HJMC_EINVAL, "need M >= 1 and x");
@@ -568,6 +588,13 @@ int hjmc_picard_solve(hjmc_handle* h, const float* x, const uint32_t* qid, uint3
       return fail(h, HJMC_ENOMEM, "picard state allocation failed");
     realloc = true;
   }
+  float* g0 = nullptr;  // g(x) for the tube epilogue (written by the init kernel)
+  if (tube) {
+    const float* old_g0 = h->d_g0;
+    if ((rc = ensure(h, &h->d_g0, &h->g0_cap, (size_t)M))) return rc;
+    realloc = realloc || h->d_g0 != old_g0;
+    g0 = h->d_g0;
+  }
   h->pic_x = x;
   h->pic_qid = qid;
   h->pic_qid_base = qid_base;
@@ -579,7 +606,7 @@ int hjmc_picard_solve(hjmc_handle* h, const float* x, const uint32_t* qid, uint3
   const std::vector<uintptr_t> key = {
       (uintptr_t)x, (uintptr_t)qid, qid_base, (uintptr_t)M, (uintptr_t)drift, tol_key,
       (uintptr_t)max_iter, (uintptr_t)v, (uintptr_t)dv, (uintptr_t)c, (uintptr_t)iters,
-      (uintptr_t)eps, (uintptr_t)dsup, h->generation,
+      (uintptr_t)eps, (uintptr_t)dsup, (uintptr_t)tube, (uintptr_t)g0, h->generation,
       // handle scratch the graph reads: another entry point may have reallocated it since
       (uintptr_t)h->d_cstate, (uintptr_t)h->d_vprev, (uintptr_t)h->d_partial,
       (uintptr_t)h->d_pstate};
@@ -597,6 +624,7 @@ int hjmc_picard_solve(hjmc_handle* h, const float* x, const uint32_t* qid, uint3
     ip.K = K;
     ip.c_state = h->d_cstate;
     ip.v_prev = h->d_vprev;
+    ip.g0 = g0;
     ip.gp.delta_eff = delta_eff(h->cfg);
     ip.gp.m0 = h->cfg.m0;
     ip.gp.c_min = h->cfg.c_min;
@@ -676,6 +704,17 @@ int hjmc_picard_solve(hjmc_handle* h, const float* x, const uint32_t* qid, uint3
     e = cudaStreamEndCapture(cap, &captured);
     if (le != cudaSuccess) return bail(le, "body launches");
     if (e != cudaSuccess) return bail(e, "body capture end");
+    // 3. after the loop: the running-min tube with the BRAT clamp over each
+    //    horizon's final iterate v[j][·]
+    if (tube) {
+      if ((e = cudaStreamBeginCaptureToGraph(cap, graph, &node, nullptr, 1,
+                                             cudaStreamCaptureModeRelaxed)) != cudaSuccess)
+        return bail(e, "tube capture");
+      le = launch_tube(g0, v, K, M, tube, x, h->cfg.n, h->avoid, cap);
+      e = cudaStreamEndCapture(cap, &captured);
+      if (le != cudaSuccess) return bail(le, "tube launch");
+      if (e != cudaSuccess) return bail(e, "tube capture end");
+    }
     cudaGraphExec_t exec = nullptr;
     if ((e = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess) return bail(e, "graph instantiate");
     h->pic_graph = graph;
@@ -688,6 +727,7 @@ int hjmc_picard_solve(hjmc_handle* h, const float* x, const uint32_t* qid, uint3
 
 int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, float* v, float* dv,
                      float* c, double* partials, void* stream) {
+  NvtxRange nvtx_range("hjmc_picard_pass");
   int rc = ready(h);
   if (rc) return rc;
   if (h->pic_M < 1) return fail(h, HJMC_EINVAL, "hjmc_picard_begin has not been called");
@@ -856,6 +896,54 @@ int hjmc_pass_count(hjmc_handle* h, void* stream, uint64_t* passes) {
 
 const char* hjmc_last_error(const hjmc_handle* h) {
   return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+int hjmc_tube(hjmc_handle* h, const float* x, int64_t M, const float* vfinal, float* tube,
+              void* stream) {
+  NvtxRange nvtx_range("hjmc_tube");
+  int rc = ready(h);
+  if (rc) return rc;
+  if (M < 0 || (M > 0 && (!x || !vfinal || !tube))) return fail(h, HJMC_EINVAL, "bad x / vfinal / tube / M");
+  if (M == 0) return HJMC_OK;
+  if ((rc = set_device(h))) return rc;
+  if ((rc = ensure(h, &h->d_g0, &h->g0_cap, (size_t)M))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  EvalParams p{};
+  p.x = x;
+  p.M = M;
+  p.g = h->d_g0;
+  p.tp = h->tp;
+  cudaError_t e = h->ks.eval_target(p, s);
+  if (e == cudaSuccess) e = launch_tube(h->d_g0, vfinal, h->cfg.K, M, tube, x, h->cfg.n, h->avoid, s);
+  if (e != cudaSuccess) return cuda_fail(h, e, "tube launch");
+  return sync_check_if_requested(h, s);
+}
+
+int hjmc_picard_decide(const double* partials, int32_t K, double tol, uint8_t* active,
+                       double* eps, double* dsup, int32_t* n_active) {
+  if (!partials || !active || K < 1 || !(tol >= 0.0)) return HJMC_EINVAL;
+  int32_t left = 0;
+  for (int j = 0; j < K; ++j) {
+    if (eps) eps[j] = NAN;
+    if (dsup) dsup[j] = NAN;
+    if (!active[j]) continue;
+    const double* q = partials + (size_t)j * 3;
+    // the same double-precision expression as the device-resident decision kernel
+    const double e = std::sqrt(q[0] / std::fmax(q[1], 1e-300));
+    if (eps) eps[j] = e;
+    if (dsup) dsup[j] = q[2];
+    if (e < tol) active[j] = 0;
+    else ++left;
+  }
+  if (n_active) *n_active = left;
+  return HJMC_OK;
+}
+
+int hjmc_residual_eps(const double* partials, int64_t count, double* eps) {
+  if (count < 0 || (count > 0 && (!partials || !eps))) return HJMC_EINVAL;
+  for (int64_t i = 0; i < count; ++i)
+    eps[i] = std::sqrt(partials[2 * i] / std::fmax(partials[2 * i + 1], 1e-300));
+  return HJMC_OK;
 }
 
 int hjmc_residual_partials(const float* vhist, const float* g0, int32_t K, int32_t Kp, int64_t M,

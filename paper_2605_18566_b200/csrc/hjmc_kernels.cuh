@@ -63,6 +63,7 @@ struct PicardInitParams {
   int K;
   double* c_state;                 // [K][M] ← Γ(x, Dg(x))
   float* v_prev;                   // [K][M] ← g(x)  (Algorithm 1: v^(0) = g)
+  float* g0;                       // [M] ← g(x) for the tube epilogue (nullable)
   GammaParams gp;
   SystemParams sp;
   TargetParams tp;

@@ -41,7 +41,10 @@ constexpr int kLgUnroll = HJMC_LG_UNROLL;
 constexpr int kGroupUnroll = HJMC_GROUP_UNROLL;  // draw groups per trip when G > 1
 constexpr double kLog2e = 1.4426950408889634074;
 constexpr double kLn2 = 0.69314718055994530942;
-constexpr float kUnderflowS = 7.888609052210118e-31f;  // 2^-100: fallback threshold
+// Two-pass fallback threshold, scaled with N. ex2.approx.ftz flushes every weight below 2^-126
+// to 0, so a pass may drop up to N·2^-126 of weight mass; falling back whenever the shifted sum
+// S < N·2^-102 keeps that loss below 2^-24 of S (one fp32 ulp) for every N (R24).
+__device__ __forceinline__ double underflow_floor(uint32_t N) { return (double)N * 0x1p-102; }
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -721,7 +724,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
           cta_reduce<NDIM, GS, NT>(sm, S, Mz, tid);
         }
       }
-      if (!(sm.sum[0] >= (double)kUnderflowS)) {
+      if (!(sm.sum[0] >= underflow_floor(P.N))) {
         // The bound-based shift left every weight tiny (or g was non-finite): redo the pass with
         // the exact maximum exponent, the plain two-pass log-sum-exp.
         float amax_t;
@@ -770,7 +773,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
         }
         // a speculative sum is kept only when a real pass at c_spec would not have needed the
         // two-pass fallback (same S, same threshold): then it equals that pass bit for bit
-        if (do_spec && sm.sum2[0] >= (double)kUnderflowS && sm.n_memo < kMemo) {
+        if (do_spec && sm.sum2[0] >= underflow_floor(P.N) && sm.n_memo < kMemo) {
           const int e = sm.n_memo;
           sm.memo_c[e] = c_spec;
           sm.memo_B[e] = B_spec;
@@ -906,6 +909,7 @@ __global__ void picard_init_kernel(const __grid_constant__ PicardInitParams P) {
   double xd[NDIM], p[NDIM];
   for (int d = 0; d < NDIM; ++d) xd[d] = (double)P.x[m * NDIM + d];
   const float g = (float)tgt.g_host(xd);
+  if (P.g0) P.g0[m] = g;
   tgt.dg(xd, p);
   const double c0 = gamma_update(P.sp, P.gp, xd, p);
   for (int j = 0; j < P.K; ++j) {

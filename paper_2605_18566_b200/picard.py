@@ -5,7 +5,9 @@ Algorithm 1 stops when ε = ‖v^(k+1) − v^(k)‖/‖v^(k)‖ < 
 over the slice's queries, R11), per horizon j. The norms are slice-wide — with queries sharded
 over GPUs the per-rank partial sums (hjmc_picard_pass) are all-reduced before the decision, so
 every rank takes the same decision. Every Φ pass and Γ update runs in the CUDA kernels; this
-module only sums six numbers per horizon and applies the stopping rule.
+module only marshals: the shards' residual partials are combined by one all-reduce (plumbing),
+and the stopping test (hjmc_picard_decide) and the tube with its BRAT clamp (hjmc_tube) run in
+the library.
 """
 from __future__ import annotations
 
@@ -58,12 +60,12 @@ def solve_adaptive(solver, x, tol: float, max_iter: int, qid_base: int = 0, qid=
     per Picard iteration (k, active horizons, ε_j(k), sup-norm differences, wall ms, max|v|,
     min/max c over the active rows; the per-iteration record of S:316–317). Returns a dict:
     v, dv, c [K][M](…) device tensors of each horizon's final iterate, iters [K],
-    eps [K][max_iter], d_sup [K][max_iter] (NaN past the stop), tube [M] = min(g, min_j v_j),
-    converged [K]."""
+    eps [K][max_iter], d_sup [K][max_iter] (NaN past the stop), tube [M] =
+    max(min(g, min_j v_j), ℓ) (hjmc_tube: running min with the BRAT clamp), converged [K]."""
     import time
     t = solver.torch
     cfg = solver.cfg
-    x = solver._as_dev(x)
+    x = solver._as_query(x)
     M, K, n = x.shape[0], cfg.K, cfg.n
     q = solver._as_dev(qid, t.int32) if qid is not None else None
     b = solver._as_dev(drift) if drift is not None else None
@@ -90,13 +92,17 @@ def solve_adaptive(solver, x, tol: float, max_iter: int, qid_base: int = 0, qid=
             solver.h, k, active.ctypes.data_as(C.c_void_p), C.c_void_p(v.data_ptr()),
             C.c_void_p(dv.data_ptr()) if dv is not None else None, C.c_void_p(c.data_ptr()),
             part.ctypes.data_as(C.c_void_p), stream))
-        tot = allreduce(part.copy()) if allreduce is not None else part
-        for j in np.flatnonzero(active):
-            iters[j] = k + 1
-            eps[j, k] = np.sqrt(tot[j, 0] / max(tot[j, 1], 1e-300))
-            dsup[j, k] = tot[j, 2]
-            if eps[j, k] < tol:
-                active[j] = 0
+        tot = np.ascontiguousarray(allreduce(part.copy()) if allreduce is not None else part)
+        iters[was_active] = k + 1
+        e_k = np.empty(K)
+        d_k = np.empty(K)
+        left = C.c_int32()
+        solver._check(L.hjmc_picard_decide(tot.ctypes.data_as(C.c_void_p), K, float(tol),
+                                           active.ctypes.data_as(C.c_void_p),
+                                           e_k.ctypes.data_as(C.c_void_p),
+                                           d_k.ctypes.data_as(C.c_void_p), C.byref(left)))
+        eps[was_active, k] = e_k[was_active]
+        dsup[was_active, k] = d_k[was_active]
         if log is not None:
             rows = t.as_tensor(was_active, device=solver.device)
             va, ca = v.index_select(0, rows), c.index_select(0, rows)
@@ -105,10 +111,11 @@ def solve_adaptive(solver, x, tol: float, max_iter: int, qid_base: int = 0, qid=
                  "d_sup": [float(dsup[j, k]) for j in was_active],
                  "ms": 1e3 * (time.perf_counter() - t0), "max_abs_v": float(va.abs().max()),
                  "c_min": float(ca.min()), "c_max": float(ca.max())})
-    g, _ = solver.eval_target(x)
-    tube = t.minimum(g, v.min(dim=0).values)
+    tube = t.empty(M, device=solver.device)
+    solver._check(L.hjmc_tube(solver.h, C.c_void_p(x.data_ptr()), M, C.c_void_p(v.data_ptr()),
+                              C.c_void_p(tube.data_ptr()), stream))
     return {"v": v, "dv": dv, "c": c, "iters": iters, "eps": eps, "d_sup": dsup, "tube": tube,
-            "converged": ~active.astype(bool), "g0": g}
+            "converged": ~active.astype(bool)}
 
 
 def torch_allreduce(group=None):
@@ -151,14 +158,13 @@ def solve_adaptive_device(solver, x, tol: float, max_iter: int, qid_base: int = 
     iters = t.zeros(K, dtype=t.int32, device=dev)
     eps = t.empty((K, max_iter), dtype=t.float64, device=dev)
     dsup = t.empty((K, max_iter), dtype=t.float64, device=dev)
+    tube = t.empty(M, device=dev)
     ptr = lambda a: C.c_void_p(a.data_ptr()) if a is not None else None
     solver._check(solver.L.hjmc_picard_solve(
         solver.h, ptr(x), ptr(q), qid_base, M, ptr(b), float(tol), int(max_iter), ptr(v), ptr(dv),
-        ptr(c), ptr(iters), ptr(eps), ptr(dsup), solver._stream()))
-    g, _ = solver.eval_target(x)
-    tube = t.minimum(g, v.min(dim=0).values)
+        ptr(c), ptr(iters), ptr(eps), ptr(dsup), ptr(tube), solver._stream()))
     eps_h = eps.cpu().numpy()
     it = iters.cpu().numpy().astype(np.int64)
     conv = np.array([it[j] > 0 and eps_h[j, it[j] - 1] < tol for j in range(K)])
     return {"v": v, "dv": dv, "c": c, "iters": it, "eps": eps_h, "d_sup": dsup.cpu().numpy(),
-            "tube": tube, "converged": conv, "g0": g}
+            "tube": tube, "converged": conv}

@@ -75,15 +75,19 @@ def solve_sharded(solve_fn: Callable, x: np.ndarray, group=None, gather: bool = 
 
 def residuals_sharded(vhist_local: np.ndarray, g0_local: np.ndarray, device=None, group=None):
     """ε_j(k) = ‖v^(k+1) − v^(k)‖₂ / ‖v^(k)‖₂ over the whole sharded slice (R11): host
-    partial sums from hjmc_residual_partials, one all-reduce (SUM) of the K·Kp·2 doubles."""
+    partial sums from hjmc_residual_partials, one all-reduce (SUM) of the K·Kp·2 doubles, then
+    hjmc_residual_eps. The all-reduce runs on the backend's device (CUDA for NCCL)."""
     import torch
     import torch.distributed as dist
 
-    from .solver import residual_partials
+    from .solver import residual_eps, residual_partials
 
     part = residual_partials(vhist_local, g0_local)          # [K][Kp][2]
-    t = torch.from_numpy(part).to(device if device is not None else "cpu")
     if dist.is_initialized():
+        if device is None:
+            device = (torch.device("cuda", torch.cuda.current_device())
+                      if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+        t = torch.from_numpy(part).to(device)
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    part = t.cpu().numpy()
-    return np.sqrt(part[..., 0] / np.maximum(part[..., 1], 1e-300))
+        part = t.cpu().numpy()
+    return residual_eps(part)

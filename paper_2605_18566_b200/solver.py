@@ -208,9 +208,12 @@ class Solver:
         return out
 
     def solve_slice_host(self, x: np.ndarray, qid_base: int = 0, drift=None, out=None,
-                         hist: bool = True):
-        """End-to-end call with HOST arrays (hjmc_solve_slice_host); synchronous."""
+                         hist: bool = True, qid=None):
+        """End-to-end call with HOST arrays (hjmc_solve_slice_host); synchronous. qid: optional
+        host array of explicit global query ids (uint32/int32, shape (M,))."""
         x = np.ascontiguousarray(x, dtype=np.float32)
+        if x.ndim != 2 or x.shape[1] != self.cfg.n:
+            raise ValueError(f"queries must have shape (M, {self.cfg.n}), got {x.shape}")
         M, n, K, Kp = x.shape[0], self.cfg.n, self.cfg.K, self.cfg.Kp
         if out is None:
             out = {"v": np.empty(M, np.float32), "dv": np.empty((M, n), np.float32),
@@ -220,12 +223,31 @@ class Solver:
                 out["vhist"] = np.empty((K, Kp, M), np.float32)
                 out["chist"] = np.empty((K, Kp, M), np.float32)
         keys = ("v", "dv", "c", "tube", "vhist", "chist", "g0")
+        # the C-ABI copies through raw host pointers: check every buffer's shape and layout
+        for k, shape in self._shapes(M).items():
+            a = out.get(k)
+            if a is None:
+                continue
+            is_t = hasattr(a, "data_ptr")
+            dt_ok = (a.dtype == self.torch.float32) if is_t else (a.dtype == np.float32)
+            contig = a.is_contiguous() if is_t else a.flags["C_CONTIGUOUS"]
+            on_host = (a.device.type == "cpu") if is_t else True
+            if tuple(a.shape) != shape or not dt_ok or not contig or not on_host:
+                raise ValueError(f"out[{k!r}] must be a contiguous host float32 array of shape "
+                                 f"{shape}, got {tuple(a.shape)} {a.dtype}")
         res = _lib.Result(*[C.c_void_p(_host_ptr(out[k])) if out.get(k) is not None else None
                             for k in keys])
         b = None if drift is None else np.ascontiguousarray(drift, dtype=np.float32)
+        if b is not None and b.shape != x.shape:
+            raise ValueError(f"drift must have the queries' shape {x.shape}")
+        q = None
+        if qid is not None:
+            q = qid if hasattr(qid, "data_ptr") else np.ascontiguousarray(qid).astype(np.uint32)
+            if tuple(q.shape) != (M,) or (hasattr(q, "is_contiguous") and not q.is_contiguous()):
+                raise ValueError(f"qid must be a contiguous host array of shape ({M},)")
         self._check(self.L.hjmc_solve_slice_host(
-            self.h, C.c_void_p(_host_ptr(x)), qid_base, M,
-            C.c_void_p(_host_ptr(b)) if b is not None else None, C.byref(res)))
+            self.h, C.c_void_p(_host_ptr(x)), C.c_void_p(_host_ptr(q)) if q is not None else None,
+            qid_base, M, C.c_void_p(_host_ptr(b)) if b is not None else None, C.byref(res)))
         return out
 
     def eval_target(self, x):
@@ -287,6 +309,19 @@ def residual_partials(vhist: np.ndarray, g0: np.ndarray) -> np.ndarray:
                                   Kp, M, C.c_void_p(out.ctypes.data))
     if rc != 0:
         raise _lib.HjmcError(rc, "residual_partials")
+    return out
+
+
+def residual_eps(partials: np.ndarray) -> np.ndarray:
+    """ε = sqrt(num / max(den, 1e-300)) per (num, den) pair (hjmc_residual_eps; P:234, R11)."""
+    L = _lib.load()
+    part = np.ascontiguousarray(partials, dtype=np.float64)
+    if part.shape[-1] != 2:
+        raise ValueError("partials must end in a (num, den) axis")
+    out = np.empty(part.shape[:-1], dtype=np.float64)
+    rc = L.hjmc_residual_eps(C.c_void_p(part.ctypes.data), out.size, C.c_void_p(out.ctypes.data))
+    if rc != 0:
+        raise _lib.HjmcError(rc, "residual_eps")
     return out
 
 

@@ -3,7 +3,14 @@ for a deterministic sample of each config's global query ids. The GPU parity tes
 same global ids through the CUDA path (results depend only on global ids, so this equals the
 full launch). Sample = an even spread, the queries nearest the target boundary band
 (|g(x)| ≤ σ_K·8.16, where the BRT boundary lies), and queries whose c^(0) is unclamped (R8).
-Usage: python scripts/make_golden.py c3 c4 c5 [--threads T]"""
+Usage: python scripts/make_golden.py c3 c4 c5 [--threads T]
+
+--chist c2: the oracle's frozen-coefficient history chist[K][Kp][M] for EVERY query of the config
+(tests/golden/<config>_chist.npz). The teacher-forced parity test feeds float32(chist[j, k]) to
+hjmc_value_grad and to the oracle's Φ at every (query, horizon, iterate),
+which isolates Φ from the Picard feedback Γ; storing c (mostly the clamp values, so it
+compresses well) instead of Φ's outputs keeps the fixture small — the test re-evaluates the
+oracle's Φ itself."""
 import math
 import os
 import sys
@@ -33,7 +40,29 @@ def sample_ids(p, P, x, n_spread, n_band, n_int):
     return np.unique(np.concatenate([spread, near, inter])).astype(np.int64)
 
 
+def chist_full(idx: int, threads: int):
+    p = I.BY_INDEX[idx]
+    P = O.Problem.from_preset(p)
+    x = I.queries(p)
+    t0 = time.time()
+    r = O.solve_slice(P, x, nthreads=threads)
+    dt = time.time() - t0
+    assert r["status"] == 0
+    path = os.path.join(ROOT, "tests", "golden", f"{p.name}_chist.npz")
+    np.savez_compressed(path, chist=r["chist"],
+                        source=np.array("scripts/make_golden.py --chist -> oracle.solve_slice "
+                                        f"(double), all {x.shape[0]} queries of preset {p.name}; "
+                                        f"{dt:.0f} s on {O.max_threads()} threads"))
+    print(f"{p.name}: chist of {x.shape[0]} queries in {dt:.0f} s -> {path}", flush=True)
+
+
 def main():
+    threads = int(sys.argv[sys.argv.index("--threads") + 1]) if "--threads" in sys.argv else 0
+    if "--chist" in sys.argv:
+        for a in sys.argv[1:]:
+            if a.startswith("c") and a[1:].isdigit():
+                chist_full(int(a[1:]), threads)
+        return
     which = [int(a.lstrip("c")) for a in sys.argv[1:] if a.startswith("c")] or [3, 4, 5]
     threads = int(sys.argv[sys.argv.index("--threads") + 1]) if "--threads" in sys.argv else 0
     for idx in which:

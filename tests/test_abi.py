@@ -52,7 +52,7 @@ def test_config_defaults_and_version(lib):
     assert (c.n, c.K, c.Kp, c.N, c.crn, c.antithetic) == (2, 1, 1, 4096, 1, 0)
     assert abs(c.m0 - 1e-3) < 1e-9 and c.c_min == pytest.approx(0.05) and c.c_max == 20.0
     assert c.seed == 0x5EED000000000001
-    assert lib.hjmc_version() == 1
+    assert lib.hjmc_version() == 2
 
 
 def test_supported_table(lib):
@@ -135,3 +135,35 @@ def test_product_package_never_imports_the_oracle():
         text = f.read_text(errors="ignore")
         assert "import oracle" not in text and "from oracle" not in text, f
         assert "liboracle" not in text and "hjmc_oracle" not in text, f
+
+
+def test_picard_decide_and_residual_eps_host(lib):
+    """Algorithm 1's stopping test behind the C-ABI (host functions, no GPU): ε_j =
+    sqrt(num / max(den, 1e-300)) on all-reduced partials (R11), retire when ε < tol,
+    NaN for inactive horizons, sup-norm difference passed through (Thm 2's d_k)."""
+    import numpy as np
+
+    part = np.array([[4.0, 100.0, 0.5], [1e-6, 1.0, 1e-3], [9.0, 0.0, 2.0], [1.0, 1.0, 7.0]])
+    active = np.array([1, 1, 1, 0], dtype=np.uint8)
+    eps = np.zeros(4)
+    dsup = np.zeros(4)
+    left = C.c_int32(-1)
+    rc = lib.hjmc_picard_decide(part.ctypes.data_as(C.c_void_p), 4, 0.01,
+                                active.ctypes.data_as(C.c_void_p), eps.ctypes.data_as(C.c_void_p),
+                                dsup.ctypes.data_as(C.c_void_p), C.byref(left))
+    assert rc == 0
+    assert eps[0] == 0.2 and eps[1] == 1e-3 and eps[2] == 3.0 / 1e-150
+    assert np.isnan(eps[3]) and np.isnan(dsup[3])
+    assert list(dsup[:3]) == [0.5, 1e-3, 2.0]
+    assert list(active) == [1, 0, 1, 0] and left.value == 2
+    # EINVAL: K < 1, negative tol, NULL partials
+    assert lib.hjmc_picard_decide(part.ctypes.data_as(C.c_void_p), 0, 0.1,
+                                  active.ctypes.data_as(C.c_void_p), None, None, None) == 1
+    assert lib.hjmc_picard_decide(part.ctypes.data_as(C.c_void_p), 4, -1.0,
+                                  active.ctypes.data_as(C.c_void_p), None, None, None) == 1
+    assert lib.hjmc_picard_decide(None, 4, 0.1, active.ctypes.data_as(C.c_void_p), None, None,
+                                  None) == 1
+    nd = np.array([[[4.0, 16.0], [0.0, 0.0]], [[2.0, 8.0], [1.0, 4.0]]])
+    out = np.zeros(4)
+    assert lib.hjmc_residual_eps(nd.ctypes.data_as(C.c_void_p), 4, out.ctypes.data_as(C.c_void_p)) == 0
+    assert list(out) == [0.5, 0.0, 0.5, 0.5]

@@ -12,6 +12,8 @@ import math
 import numpy as np
 import pytest
 
+from paper_2605_18566_b200 import inputs as I
+
 
 def test_dubins_spec_cases(oracle_mod):
     O = oracle_mod
@@ -374,3 +376,24 @@ def test_picard_follows_quadrature_picard(oracle_mod):
     for m, (q, cs, vs, ses) in enumerate(kept):
         np.testing.assert_array_equal(r["chist"][j - 1, :, m], cs)
         assert np.all(np.abs(r["vhist"][j - 1, :, m] - vs) <= 5 * np.array(ses) + 1e-9), q
+
+
+def test_oracle_tube_matches_solve_slice_tube(oracle_mod):
+    """orc_tube (used for Algorithm 1 with its stopping test) is the same running-min tube with
+    the BRAT clamp as orc_solve_slice's: identical on the fixed schedule, ≤ g and
+    ≤ every horizon's final iterate without an obstacle, ≥ ℓ with one."""
+    O = oracle_mod
+    p = I.PAPER_DOUBLE_INTEGRATOR.with_(N=600, K=2, Kp=3)
+    x = I.queries(p)[::41]
+    for pa in (p, p.with_(avoid="disk", avoid_params=(0.3, -0.2, 0.4))):
+        P = O.Problem.from_preset(pa)
+        fixed = O.solve_slice(P, x)
+        ad = O.picard_adaptive(P, x, 0.0, 3)
+        np.testing.assert_array_equal(ad["v"], fixed["vhist"][:, -1])
+        np.testing.assert_array_equal(ad["tube"], fixed["tube"])
+        ell = np.array([O.avoid_l(P, xm.astype(np.float64)) for xm in x])
+        assert np.all(ad["tube"] >= ell)
+        if pa.avoid == "none":
+            assert np.all(ad["tube"] <= fixed["g0"]) and np.all(ad["tube"] <= ad["v"].min(0))
+        else:
+            assert np.any(ad["tube"] == ell)               # the clamp binds somewhere
