@@ -10,7 +10,11 @@ Usage: python scripts/make_golden.py c3 c4 c5 [--threads T]
 hjmc_value_grad and to the oracle's Φ at every (query, horizon, iterate),
 which isolates Φ from the Picard feedback Γ; storing c (mostly the clamp values, so it
 compresses well) instead of Φ's outputs keeps the fixture small — the test re-evaluates the
-oracle's Φ itself."""
+oracle's Φ itself.
+
+--teacher c3 c4 c5: the oracle's Φ at every unique (query, horizon, float32 c) of the sampled
+C3–C5 trajectories (tests/golden/<config>_teacher.npz), for the same teacher-forced test at full
+size without re-running minutes of oracle work per test run."""
 import math
 import os
 import sys
@@ -56,8 +60,53 @@ def chist_full(idx: int, threads: int):
     print(f"{p.name}: chist of {x.shape[0]} queries in {dt:.0f} s -> {path}", flush=True)
 
 
+def teacher_items(chist):
+    """Unique (query index m, horizon j (0-based), float32 c) over every iterate k of
+    chist[K][Kp][M] — under CRN a Φ pass is a function of (m, j, c) alone."""
+    K, Kp, M = chist.shape
+    cf = chist.astype(np.float32)
+    items = sorted({(m, j, float(cf[j, k, m])) for j in range(K) for k in range(Kp) for m in range(M)})
+    m = np.array([t[0] for t in items], dtype=np.int64)
+    j = np.array([t[1] for t in items], dtype=np.int64)
+    c = np.array([t[2] for t in items], dtype=np.float32)
+    return m, j, c
+
+
+def teacher_tau(p, j0):
+    """τ_j as the fp32 value hjmc_value_grad receives (j0 = 0-based horizon)."""
+    return np.float32((j0 + 1) * p.T / p.K)
+
+
+def teacher(idx: int, threads: int):
+    """Teacher-forced Φ of the oracle at its OWN coefficient history:
+    for every unique (query, horizon, float32(chist[j, k])) of the <config>_sample.npz ids, v and
+    Dv of one pass at that c, τ = float32(j T/K), counter tags (j, 0) (CRN). The GPU test feeds
+    the same c to hjmc_value_grad at every (j, k), isolating Φ from the Picard feedback."""
+    p = I.BY_INDEX[idx]
+    P = O.Problem.from_preset(p)
+    assert p.crn
+    d = np.load(os.path.join(ROOT, "tests", "golden", f"{p.name}_sample.npz"))
+    m, j, c = teacher_items(d["chist"])
+    tau = np.array([teacher_tau(p, jj) for jj in j], dtype=np.float64)
+    t0 = time.time()
+    v, dv = O.phi_items(P, d["x"], m, d["ids"][m].astype(np.uint32), c.astype(np.float64), tau,
+                        (j + 1).astype(np.uint32), 0, nthreads=threads)
+    dt = time.time() - t0
+    path = os.path.join(ROOT, "tests", "golden", f"{p.name}_teacher.npz")
+    np.savez_compressed(path, m=m, j=j, c=c, v=v, dv=dv,
+                        source=np.array("scripts/make_golden.py --teacher -> oracle.phi_items "
+                                        f"(double) at float32(chist) of {p.name}_sample.npz; "
+                                        f"{len(m)} passes, {dt:.0f} s on {O.max_threads()} threads"))
+    print(f"{p.name}: {len(m)} teacher-forced passes in {dt:.0f} s -> {path}", flush=True)
+
+
 def main():
     threads = int(sys.argv[sys.argv.index("--threads") + 1]) if "--threads" in sys.argv else 0
+    if "--teacher" in sys.argv:
+        for a in sys.argv[1:]:
+            if a.startswith("c") and a[1:].isdigit():
+                teacher(int(a[1:]), threads)
+        return
     if "--chist" in sys.argv:
         for a in sys.argv[1:]:
             if a.startswith("c") and a[1:].isdigit():

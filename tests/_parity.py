@@ -113,17 +113,39 @@ def propagated_bounds(O, P, x, qid, j, c_ref, v_ref, dv_ref, floor):
     return bv, bc, bd
 
 
-def assert_picard_history(O, P, x, qids, vhist_gpu, chist_gpu, ref):
+# R27 allowance, capped at the rates measured on the complete C2 slice (round 1: 1 of 102,010
+# (query, horizon) units and 2 of 10,201 final outputs needed the propagated bound): at most
+# 0.1 % of units and 0.05 % of final outputs — at least one, for the small sampled sets that
+# deliberately include the interior-c band (R8) where Γ is expansive.
+R27_UNIT_FRAC = 1e-3
+R27_OUTPUT_FRAC = 5e-4
+
+
+def r27_cap(count, frac):
+    return max(1, int(frac * count))
+
+
+def assert_picard_history(O, P, x, qids, vhist_gpu, chist_gpu, ref, what=""):
     """vhist and chist at every (j, k): the plain R20 / R25 checks, and for a (query, horizon)
     that fails them, the propagated non-contractive bound above. Returns the number of
-    (query, horizon) pairs that needed the propagated bound."""
+    (query, horizon) pairs that needed the propagated bound, which must stay within the R27 cap
+    (printed, with the ids)."""
     x = np.asarray(x, dtype=np.float64)
     M = x.shape[0]
     floor = FLOOR * np.abs(ref["vhist"]).max()
     dg = np.stack([O.dg(P, xm) for xm in x])
+    # vectorised pre-check: units whose every iterate passes plain R20 on v and c's base term
+    # need no per-iterate work (c_violations' first test is exactly the base term)
+    vr, cr = np.asarray(ref["vhist"]), np.asarray(ref["chist"])
+    vg = np.asarray(vhist_gpu, dtype=np.float64)
+    cg = np.asarray(chist_gpu, dtype=np.float64)
+    quick = ((np.abs(vg - vr) <= V_RTOL * np.maximum(np.abs(vr), floor))
+             & (np.abs(cg - cr) <= V_RTOL * np.abs(cr))).all(axis=1)        # [K][M]
     needed = 0
     for m in range(M):
         for j in range(P.K):
+            if quick[j, m]:
+                continue
             base_ok = True
             for k in range(P.Kp):
                 vr = ref["vhist"][j, k, m]
@@ -138,6 +160,7 @@ def assert_picard_history(O, P, x, qids, vhist_gpu, chist_gpu, ref):
             if base_ok:
                 continue
             needed += 1
+            print(f"R27 {what}: query {int(qids[m])} horizon {j + 1} judged by the propagated bound")
             bv, bc, _ = propagated_bounds(O, P, x[m], qids[m], j + 1, ref["chist"][j, :, m],
                                        ref["vhist"][j, :, m], ref["dvhist"][j, :, m], floor)
             for k in range(P.Kp):
@@ -146,4 +169,55 @@ def assert_picard_history(O, P, x, qids, vhist_gpu, chist_gpu, ref):
                 assert dv <= bv[k] and dc <= bc[k], (
                     f"query {qids[m]} horizon {j} iterate {k}: |Δv| {dv:.3g} (bound {bv[k]:.3g}), "
                     f"|Δc| {dc:.3g} (bound {bc[k]:.3g})")
+    units = M * P.K
+    print(f"R27 {what}: {needed} of {units} (query, horizon) units needed the propagated bound "
+          f"(cap {r27_cap(units, R27_UNIT_FRAC)})")
+    assert needed <= r27_cap(units, R27_UNIT_FRAC), f"{needed} units needed the R27 band"
     return needed
+
+
+def _final_outputs_within(O, P, x, qids, g, ref, sel=None):
+    """v, Dv and tube at τ_K: R20, except for queries whose last horizon is non-contractive,
+    which are covered by assert_picard_history's propagated bound on vhist[K−1][Kp−1] (= v)."""
+    take = (lambda a: a[sel]) if sel is not None else (lambda a: a)
+    vg, dvg, tg = take(g["v"]), take(g["dv"]), take(g["tube"])
+    okv = v_violations(vg, ref["v"]) <= 1.0
+    okd = dv_violations(dvg, ref["dv"]) <= 1.0
+    okt = v_violations(tg, ref["tube"]) <= 1.0
+    bad = np.flatnonzero(~(okv & okd & okt))
+    floor = 1e-2 * np.abs(ref["vhist"]).max()
+    for m in bad:                                   # must be explained by the propagated bound
+        bv, _, bd = propagated_bounds(O, P, x[m], qids[m], P.K, ref["chist"][-1, :, m],
+                                      ref["vhist"][-1, :, m], ref["dvhist"][-1, :, m], floor)
+        assert abs(vg[m] - ref["v"][m]) <= bv[-1], f"v at query {qids[m]}"
+        assert np.linalg.norm(dvg[m] - ref["dv"][m]) <= bd[-1], f"Dv at query {qids[m]}"
+        assert abs(tg[m] - ref["tube"][m]) <= max(bv[-1], 2e-4 * max(abs(ref["tube"][m]), floor))
+    print(f"R27: {len(bad)} of {len(vg)} final outputs judged by the propagated bound "
+          f"(ids {[int(qids[m]) for m in bad]}; cap {r27_cap(len(vg), R27_OUTPUT_FRAC)})")
+    assert len(bad) <= r27_cap(len(vg), R27_OUTPUT_FRAC), f"{len(bad)} queries outside R20 at τ_K"
+
+
+# Teacher forcing (VERDICT r1, item 1b): Φ alone at the oracle's OWN coefficient history. Under
+# common random numbers a pass is a function of (query, horizon, c), so every iterate (j, k) of a
+# trajectory maps to one item (m, j, float32(chist[j, k, m])); both sides evaluate Φ there with
+# τ_j as the fp32 value hjmc_value_grad receives and counter tags (j + 1, 0).
+def teacher_items(chist):
+    """Unique (m, j, float32 c) items of chist[K][Kp][M] and, per (j, k, m), the item index."""
+    K, Kp, M = chist.shape
+    cf = np.asarray(chist).astype(np.float32)
+    keys = {}
+    index = np.zeros((K, Kp, M), dtype=np.int64)
+    for j in range(K):
+        for k in range(Kp):
+            for m, c in enumerate(cf[j, k].tolist()):
+                index[j, k, m] = keys.setdefault((m, j, c), len(keys))
+    items = sorted(keys, key=keys.get)
+    m = np.array([t[0] for t in items], dtype=np.int64)
+    j = np.array([t[1] for t in items], dtype=np.int64)
+    c = np.array([t[2] for t in items], dtype=np.float32)
+    return m, j, c, index
+
+
+def teacher_tau(T, K, j0):
+    """τ_j (j0 = 0-based horizon) as the fp32 value hjmc_value_grad receives."""
+    return np.float32((j0 + 1) * T / K)

@@ -303,3 +303,45 @@ def test_tilted_agrees_with_plain_on_games(oracle_mod):
         vt, dvt, dt, st = O.phi(O.Problem(**kw, proposal="laplace"), x, c, tau, qid=5)
         assert abs(vp - vt) < KSE * math.hypot(dp[3], dt[3])
         assert np.all(np.abs(dvp - dvt) < KSE * np.hypot(sp, st) + 1e-9)
+
+
+# ---- the oracle's statistical yardstick ---------------------------------
+@pytest.mark.parametrize("case", ["bowl", "disk", "pair_union"])
+def test_standard_errors_match_seed_spread(oracle_mod, case):
+    """Pin of orc_phi's delta-method standard errors — diag[3] for v̂ and se_dv for each Dv̂
+    component — which set the width of every MC-vs-quadrature pin above. Thm 1
+    makes v̂ a sample-mean functional with O(N^-½) spread; over R = 2048 independent seeds at a
+    fixed (x, c, τ) the empirical standard deviation of v̂ and of every Dv̂ component must match
+    the mean of the per-run SE estimates within ±10 %: the χ² 99.9 % band of a 2048-sample
+    standard deviation is ±5.1 %, the rest covers the O(1/N) delta-method bias. A dropped 1/c,
+    1/σ or √N, or S in place of S², misses by a factor ≥ √2."""
+    O = oracle_mod
+    if case == "bowl":
+        kw = dict(n=2, delta=0.05, visc="paper", system="quadratic", target="quad_bowl",
+                  tgt_params=(0.25,))
+        x, c, tau = np.array([0.3, -0.2]), 20.0, 0.2
+    elif case == "disk":
+        kw = dict(n=2, delta=0.01, system="quadratic", target="disk", tgt_params=(1.0,))
+        x, c, tau = np.array([1.1, 0.4]), 6.0, 1.0
+    else:
+        kw = dict(n=15, delta=0.02, system="dubins_pairs", target="pair_union", tgt_params=(1.0,))
+        x = np.zeros(15)
+        x[0], x[1], x[3], x[4] = 1.3, 0.2, 0.9, -1.2
+        x[6:] = np.tile([4.0, 0.0, 0.0], 3)
+        c, tau = 3.0, 1.0
+    R, N = 2048, 4096
+    v = np.zeros(R)
+    dv = np.zeros((R, x.size))
+    se_v = np.zeros(R)
+    se_dv = np.zeros((R, x.size))
+    for r in range(R):
+        P = O.Problem(N=N, seed=0xC0FFEE00 + 7919 * r, **kw)
+        v[r], dv[r], diag, se_dv[r] = O.phi(P, x, c, tau, qid=r, jw=1, kw=0)
+        se_v[r] = diag[3]
+    lo, hi = stats.chi2.ppf([5e-4, 1 - 5e-4], R - 1) / (R - 1)
+    assert 0.94 < math.sqrt(lo) and math.sqrt(hi) < 1.06          # the ±5.1 % band, R = 2048
+    ratio_v = v.std(ddof=1) / se_v.mean()
+    ratio_dv = dv.std(axis=0, ddof=1) / se_dv.mean(axis=0)
+    print(f"{case}: std/SE v {ratio_v:.4f}, Dv {np.round(ratio_dv, 4)}")
+    assert abs(ratio_v - 1.0) < 0.10, ratio_v
+    assert np.all(np.abs(ratio_dv - 1.0) < 0.10), ratio_dv

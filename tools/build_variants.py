@@ -19,6 +19,15 @@ VARIANTS = {
     "mb4": ["-DHJMC_MINB=4"],
     "mb5": ["-DHJMC_MINB=5"],
     "mb6": ["-DHJMC_MINB=6"],
+    # lane-group kernel (n = 37–48): one sample per trip (the round-1 kernel) at 4 / 3 CTAs per
+    # SM, two samples per trip (the default) at 4 / 3 CTAs per SM. Measured on the C5 benchmark
+    # queries (1,184, full N/K/Kp): 4500 / 4451 / 4680 / 4713 ms vs the default's 4409 ms. Round 1's
+    # Philox round-1 product kept by 64-bit addition (one IMAD.WIDE fewer per lane-trip) measured
+    # 4478 / 4431 ms (single / dual) and was removed.
+    "single4": ["-DHJMC_LG_DUAL=0", "-DHJMC_MINB=4"],
+    "single3": ["-DHJMC_LG_DUAL=0", "-DHJMC_MINB=3"],
+    "dual4": ["-DHJMC_LG_DUAL=1", "-DHJMC_MINB=4"],
+    "dual3": ["-DHJMC_LG_DUAL=1", "-DHJMC_MINB=3"],
 }
 
 if __name__ == "__main__":

@@ -11,7 +11,12 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from paper_2605_18566_b200 import inputs as I  # noqa: E402
+from paper_2605_18566_b200 import _lib, inputs as I  # noqa: E402
+
+if "--lib" in sys.argv:               # a build variant (tools/build_variants.py)
+    i = sys.argv.index("--lib")
+    _lib.load(sys.argv[i + 1])
+    del sys.argv[i:i + 2]
 from paper_2605_18566_b200.solver import Solver, SolverConfig  # noqa: E402
 
 if __name__ == "__main__":
@@ -21,7 +26,8 @@ if __name__ == "__main__":
     Kp = int(sys.argv[4]) if len(sys.argv) > 4 else 1
     p = I.BY_INDEX[idx].with_(K=K, Kp=Kp)
     x_all = I.queries(I.BY_INDEX[idx])
-    ids = I.subsample_ids(x_all.shape[0], nq)
+    ids = I.bench_ids(I.BY_INDEX[idx])          # the benchmark's queries (C5: its subset)
+    ids = ids[np.linspace(0, len(ids) - 1, min(nq, len(ids))).round().astype(int)]
     s = Solver(SolverConfig.from_preset(p))
     x = torch.from_numpy(x_all[ids]).cuda()
     qid = torch.from_numpy(ids.astype(np.int32)).cuda()
