@@ -28,6 +28,9 @@ VARIANTS = {
     "single3": ["-DHJMC_LG_DUAL=0", "-DHJMC_MINB=3"],
     "dual4": ["-DHJMC_LG_DUAL=1", "-DHJMC_MINB=4"],
     "dual3": ["-DHJMC_LG_DUAL=1", "-DHJMC_MINB=3"],
+    "rng6": ["-DHJMC_RNG6_PROTO=1"],          # timing prototype only (not the contract)
+    "pipe": ["-DHJMC_LG_PIPE=1"],
+    "pipe6": ["-DHJMC_LG_PIPE=1", "-DHJMC_RNG6_PROTO=1"],
 }
 
 if __name__ == "__main__":
