@@ -275,9 +275,6 @@ constexpr int kLgLanes = HJMC_LG_LANES;
 #ifndef HJMC_LG_DUAL
 #define HJMC_LG_DUAL 1
 #endif
-#ifndef HJMC_LG_PIPE
-#define HJMC_LG_PIPE 0
-#endif
 constexpr bool kLgDual = HJMC_LG_DUAL != 0;  // two samples per lane-group trip (lg_pass)
 
 constexpr int kLgSpan = 48 / kLgLanes;
@@ -314,40 +311,16 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
 #pragma unroll
   for (int c = 0; c < kLgSpan; ++c) Mb[c] = 0.f;
   const uint32_t N = P.N;
-  // this lane's 12 normals of sample i (its Philox blocks kBlocks·l .. kBlocks·l + kBlocks − 1),
-  // in two steps: the raw Philox words, then the Box–Muller transform
-#if HJMC_RNG6_PROTO
-  constexpr int kRaw = 2;                               // PROTOTYPE: 6 normals per block
-#else
-  constexpr int kRaw = kBlocks;
-#endif
-  auto raw = [&](uint32_t i, uint4 (&W)[kRaw]) {
+  // this lane's 12 normals of sample i (its Philox blocks kBlocks·l .. kBlocks·l + kBlocks − 1)
+  auto draw = [&](uint32_t i, float (&z)[kLgSpan]) {
 #pragma unroll
-    for (int qd = 0; qd < kRaw; ++qd)
-      W[qd] = philox4x32_10(i, w1base | (uint32_t)(kRaw * l + qd), qid, P.tag, P.rk);
-  };
-  auto transform = [&](const uint4 (&W)[kRaw], float (&z)[kLgSpan]) {
-#pragma unroll
-    for (int qd = 0; qd < kRaw; ++qd) {
-      const uint4 w = W[qd];
-#if HJMC_RNG6_PROTO
-      const uint32_t a0 = w.w & 0xFFFFE000u;
-      const uint32_t a1 = (w.w << 19) | ((w.x & 0x1FFu) << 10);
-      const uint32_t a2 = ((w.y & 0x1FFu) << 23) | ((w.z & 0x1FFu) << 14);
-      box_muller_hat<true>(w.x, a0, z[6 * qd], z[6 * qd + 1]);
-      box_muller_hat<true>(w.y, a1, z[6 * qd + 2], z[6 * qd + 3]);
-      box_muller_hat<true>(w.z, a2, z[6 * qd + 4], z[6 * qd + 5]);
-#else
+    for (int qd = 0; qd < kBlocks; ++qd) {
+      const uint4 w = philox4x32_10(i, w1base | (uint32_t)(kBlocks * l + qd), qid, P.tag, P.rk);
       box_muller_hat<true>(w.x, w.y, z[4 * qd], z[4 * qd + 1]);
       box_muller_hat<true>(w.z, w.w, z[4 * qd + 2], z[4 * qd + 3]);
-#endif
     }
   };
-  auto draw = [&](uint32_t i, float (&z)[kLgSpan]) {
-    uint4 W[kRaw];
-    raw(i, W);
-    transform(W, z);
-  };
+
 
   // min over this lane's (x, y) pairs of |pos|² (pursuit: |pursuer − evader|²)
   auto partial_min = [&](const float (&z)[kLgSpan]) -> float {
@@ -412,32 +385,10 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
     // The min is exact and each weight is formed from the same fp32 values by the same MUFU
     // ops, and S, Mb accumulate w_t then w_{t+1} as the one-sample loop does: bit-identical.
     const bool lo = l < 2;
-#if HJMC_LG_PIPE
-    // software pipeline: the next pair's Philox words are generated in the same loop body as
-    // this pair's Box–Muller transforms, so each warp's instruction stream mixes the IMAD-heavy
-    // and the MUFU-heavy work instead of alternating phases (the last body computes one unused
-    // pair — Philox is a pure function of the counter)
-    uint4 W0[kRaw], W1[kRaw];
-    raw(t0 * kStride + slot, W0);
-    raw((t0 + 1) * kStride + slot, W1);
-#endif
     for (; t0 + 1 < full; t0 += 2) {
       float z0[kLgSpan], z1[kLgSpan];
-#if HJMC_LG_PIPE
-      uint4 N0[kRaw], N1[kRaw];
-      raw((t0 + 2) * kStride + slot, N0);
-      raw((t0 + 3) * kStride + slot, N1);
-      transform(W0, z0);
-      transform(W1, z1);
-#pragma unroll
-      for (int qd = 0; qd < kRaw; ++qd) {
-        W0[qd] = N0[qd];
-        W1[qd] = N1[qd];
-      }
-#else
       draw(t0 * kStride + slot, z0);
       draw((t0 + 1) * kStride + slot, z1);
-#endif
       const float b0 = partial_min(z0), b1 = partial_min(z1);
       float mine = lo ? b0 : b1;
       const float other = lo ? b1 : b0;

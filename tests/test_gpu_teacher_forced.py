@@ -26,6 +26,11 @@ from paper_2605_18566_b200.solver import Solver, SolverConfig  # noqa: E402
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
+@pytest.fixture(scope="module")
+def O(oracle_mod):
+    return oracle_mod
+
+
 def _forced_passes(s, p, x, chist, index, v_ref, dv_ref, qid=None):
     """GPU value_grad at every (j, k) of chist; returns the worst v and Dv ratios per (j, k)."""
     K, Kp, M = chist.shape

@@ -28,10 +28,13 @@ VARIANTS = {
     "single3": ["-DHJMC_LG_DUAL=0", "-DHJMC_MINB=3"],
     "dual4": ["-DHJMC_LG_DUAL=1", "-DHJMC_MINB=4"],
     "dual3": ["-DHJMC_LG_DUAL=1", "-DHJMC_MINB=3"],
-    "rng6": ["-DHJMC_RNG6_PROTO=1"],          # timing prototype only (not the contract)
-    "pipe": ["-DHJMC_LG_PIPE=1"],
-    "pipe6": ["-DHJMC_LG_PIPE=1", "-DHJMC_RNG6_PROTO=1"],
 }
+# Also measured this round and removed from the source (same queries, same box): a software-
+# pipelined dual loop (the next pair's Philox words generated in the body that transforms this
+# pair) 4908 ms vs 4417 ms; a prototype draw layout with 6 normals per Philox block (3 Box–Muller
+# pairs from 128 bits: 30 % fewer IMAD.WIDE) 4259 ms, pipelined 4201 ms — 4–5 %, too little to
+# change the frozen sampler contract (R19) and every golden fixture for: the kernel is bound by
+# the MUFU/issue co-limit, not by the wide multiplies alone.
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
