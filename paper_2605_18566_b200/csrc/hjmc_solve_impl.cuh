@@ -283,7 +283,7 @@ static_assert(kLgLanes == 2 || kLgLanes == 4, "lane groups of 2 or 4");
 // Speculative sums of the lane-group pass (HJMC_FLAG_SPECULATE_CLAMPS): the same samples at a
 // second coefficient, weight 2^(A·core + B).
 struct LgSpec {
-  float A, B, S, Mb[kLgSpan];
+  float A, B, S, S1, Mb[kLgSpan];
 };
 
 template <int NDIM, int NT, bool kMaxMode, bool kPursuit = false, bool kSpec = false>
@@ -351,7 +351,14 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
   };
   // One sample per lane group per trip; trips where every slot's sample exists run without
   // the i < N guard (C5: N = 2^20, all of them), the ragged last trip with it.
-  auto trip = [&](uint32_t i, bool guard) {
+  // The weight sum is split by trip parity into two fp32 accumulators (S for even trips, S1 for
+  // odd ones, added at the end): a lane group sums N/64 = 16,384 weights per pass at C5, and at
+  // c = c_min (weights ≈ 1) one accumulator's rounding walk reaches ~5e-6 relative, which
+  // v = −log(S/N)/c amplifies by 1/c = 20 (R20 allows 5e-5 absolute near v = 0). Two halves cut
+  // that by 2√2 at no cost in the loop; every path (one- or two-sample trips, speculative sums)
+  // uses the same split, so a speculative pass still equals a real one bit for bit.
+  float S1 = 0.f;
+  auto trip = [&](uint32_t i, bool guard, bool odd) {
     float z[kLgSpan];
     draw(i, z);
     float best = partial_min(z);
@@ -363,12 +370,14 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
         amax = fmaxf(amax, A * core);
       } else {
         const float wt = ex2_approx(fmaf(A, core, B));
-        S += wt;
+        if (odd) S1 += wt;
+        else S += wt;
 #pragma unroll
         for (int c = 0; c < kLgSpan; ++c) Mb[c] = fmaf(wt, z[c], Mb[c]);
         if constexpr (kSpec) {
           const float w2 = ex2_approx(fmaf(sp->A, core, sp->B));
-          sp->S += w2;
+          if (odd) sp->S1 += w2;
+          else sp->S += w2;
 #pragma unroll
           for (int c = 0; c < kLgSpan; ++c) sp->Mb[c] = fmaf(w2, z[c], sp->Mb[c]);
         }
@@ -397,17 +406,19 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
       const float wm = ex2_approx(fmaf(A, sqrt_approx(mine), B));
       const float wo = __shfl_xor_sync(0xffffffffu, wm, 2);
       const float w0 = lo ? wm : wo, w1 = lo ? wo : wm;
-      S += w0;
+      S += w0;                                                     // t0 even
 #pragma unroll
       for (int c = 0; c < kLgSpan; ++c) Mb[c] = fmaf(w0, z0[c], Mb[c]);
-      S += w1;
+      S1 += w1;                                                    // t0 + 1 odd
 #pragma unroll
       for (int c = 0; c < kLgSpan; ++c) Mb[c] = fmaf(w1, z1[c], Mb[c]);
     }
   }
 #pragma unroll(kLgUnroll)
-  for (uint32_t t = t0; t < full; ++t) trip(t * kStride + slot, false);
-  if (full * kStride < N) trip(full * kStride + slot, true);
+  for (uint32_t t = t0; t < full; ++t) trip(t * kStride + slot, false, t & 1u);
+  if (full * kStride < N) trip(full * kStride + slot, true, full & 1u);
+  S += S1;
+  if constexpr (kSpec) sp->S += sp->S1;
 }
 
 // Merge the lane-group sums into sm.sum (double), deterministic order.
@@ -730,6 +741,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
             __syncthreads();
             sp.B = opaque(sm.lg_B2);
             sp.S = 0.f;
+            sp.S1 = 0.f;
 #pragma unroll
             for (int c2 = 0; c2 < kLgSpan; ++c2) sp.Mb[c2] = 0.f;
             lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit, true>(
