@@ -49,11 +49,23 @@ class _Problem(C.Structure):
 _lib = None
 
 
+def build_sanitized(path: str = os.path.join(HERE, "liboracle_san.so")) -> str:
+    """The same oracle compiled with -fsanitize=address,undefined (tools/sanitize_oracle.sh runs
+    the CPU suite against it with HJMC_ORACLE_LIB=<path> and libasan preloaded)."""
+    cmd = ["gcc", "-O1", "-g", "-std=c11", "-fopenmp", "-fPIC", "-shared",
+           "-fsanitize=address,undefined", "-fno-sanitize-recover=undefined",
+           "-fno-omit-frame-pointer", "-o", path, SRC, "-lm"]
+    subprocess.run(cmd, check=True)
+    return path
+
+
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(LIB)
+        path = os.environ.get("HJMC_ORACLE_LIB")
+        if not path:
+            build()
+        L = C.CDLL(path or LIB)
         dp, fp, up = C.POINTER(C.c_double), C.POINTER(C.c_float), C.POINTER(C.c_uint32)
         pp = C.POINTER(_Problem)
         L.orc_philox4x32_10.argtypes = [up, up, up]

@@ -24,8 +24,9 @@ def curand_host(tmp_path_factory):
     if not os.path.exists(nvcc):
         pytest.skip("nvcc not available to build the curand host reference")
     exe = str(tmp_path_factory.mktemp("cph") / "cph")
+    env = {k: v for k, v in os.environ.items() if k != "LD_PRELOAD"}   # (sanitizer runs)
     subprocess.run([nvcc, "-O1", "-Wno-deprecated-gpu-targets", "-o", exe,
-                    os.path.join(HERE, "tools", "curand_philox_host.cu")], check=True)
+                    os.path.join(HERE, "tools", "curand_philox_host.cu")], check=True, env=env)
     return exe
 
 
@@ -34,7 +35,9 @@ def test_philox_bit_exact_vs_curand(oracle_mod, curand_host):
     cases = [[0, 0, 0, 0, 0, 0], [0xFFFFFFFF] * 6]
     cases += rng.integers(0, 2**32, size=(254, 6), dtype=np.uint64).tolist()
     inp = "\n".join(" ".join(str(int(v)) for v in c) for c in cases) + "\n"
-    out = subprocess.run([curand_host], input=inp, capture_output=True, text=True, check=True)
+    env = {k: v for k, v in os.environ.items() if k != "LD_PRELOAD"}
+    out = subprocess.run([curand_host], input=inp, capture_output=True, text=True, check=True,
+                         env=env)
     ref = [list(map(int, ln.split())) for ln in out.stdout.strip().splitlines()]
     assert len(ref) == len(cases)
     for c, r in zip(cases, ref):
