@@ -328,6 +328,20 @@ HJMC_API int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, 
 HJMC_API int hjmc_picard_decide(const double* partials, int32_t K, double tol, uint8_t* active,
                                 double* eps, double* dsup, int32_t* n_active);
 
+/* Theorem 2's contraction constant (Eq. contraction_const; R18 reads 2G/c_min):
+ *   q = (2G/c_min) · (2 L_D/δ) · (L_H/m0² + 2 H_star P_star / m0⁴).  Host-only, no handle. */
+HJMC_API double hjmc_contraction_constant(double G, double c_min, double L_D, double delta, double L_H,
+                                          double m0, double H_star, double P_star);
+
+/* Theorem 2 diagnostics from the sup-norm Picard differences d[0..count−1]
+ * (d_k = ‖v^(k+1) − v^(k)‖∞, e.g. hjmc_picard_solve's dsup row): q_hat[k] = d[k+1]/d[k] for
+ * k < count − 1 (IEEE division: 0/0 = NaN, x/0 = ±inf); when 0 ≤ q < 1 the a-posteriori bound
+ * apost[k] = q/(1−q)·d[k] on ‖v^(k+1) − v*‖∞ (Eq. aposteriori-error) is written
+ * and 1 is returned (certified), else apost is untouched and 0 is returned. q_hat / apost may
+ * be NULL; −1 (EINVAL-like) for count < 0 or NULL d with count > 0. Host-only. */
+HJMC_API int hjmc_contraction_report(const double* d, int64_t count, double q, double* q_hat,
+                                     double* apost);
+
 /* Post-hoc residuals (a12; R11) from summed partials (HOST [count][2] = (num, den), e.g.
  * hjmc_residual_partials all-reduced over shards): eps[i] = sqrt(num / max(den, 1e-300)). */
 HJMC_API int hjmc_residual_eps(const double* partials, int64_t count, double* eps);

@@ -32,6 +32,7 @@ EXPORTS = [
     "hjmc_last_bad_query", "hjmc_last_error", "hjmc_residual_partials", "hjmc_version",
     "hjmc_pass_count", "hjmc_picard_begin", "hjmc_picard_pass", "hjmc_picard_solve",
     "hjmc_set_avoid", "hjmc_picard_decide", "hjmc_residual_eps", "hjmc_tube",
+    "hjmc_contraction_constant", "hjmc_contraction_report",
 ]
 
 
@@ -99,6 +100,10 @@ def load(path: str = LIB_PATH):
     L.hjmc_picard_decide.argtypes = [vp, C.c_int32, C.c_double, vp, vp, vp, vp]
     L.hjmc_residual_eps.argtypes = [vp, i64, vp]
     L.hjmc_tube.argtypes = [vp, vp, i64, vp, vp, vp]
+    dd = C.c_double
+    L.hjmc_contraction_constant.argtypes = [dd] * 8
+    L.hjmc_contraction_constant.restype = dd
+    L.hjmc_contraction_report.argtypes = [vp, i64, dd, vp, vp]
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"libhjmc.so lacks {name}")

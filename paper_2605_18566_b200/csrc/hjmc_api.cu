@@ -939,6 +939,23 @@ int hjmc_picard_decide(const double* partials, int32_t K, double tol, uint8_t* a
   return HJMC_OK;
 }
 
+double hjmc_contraction_constant(double G, double c_min, double L_D, double delta, double L_H,
+                                 double m0, double H_star, double P_star) {
+  return (2.0 * G / c_min) * (2.0 * L_D / delta) *
+         (L_H / (m0 * m0) + 2.0 * H_star * P_star / (m0 * m0 * m0 * m0));
+}
+
+int hjmc_contraction_report(const double* d, int64_t count, double q, double* q_hat,
+                            double* apost) {
+  if (count < 0 || (count > 0 && !d)) return -1;
+  if (q_hat)
+    for (int64_t k = 0; k + 1 < count; ++k) q_hat[k] = d[k + 1] / d[k];
+  const bool certified = q >= 0.0 && q < 1.0;
+  if (certified && apost)
+    for (int64_t k = 0; k < count; ++k) apost[k] = q / (1.0 - q) * d[k];
+  return certified ? 1 : 0;
+}
+
 int hjmc_residual_eps(const double* partials, int64_t count, double* eps) {
   if (count < 0 || (count > 0 && (!partials || !eps))) return HJMC_EINVAL;
   for (int64_t i = 0; i < count; ++i)

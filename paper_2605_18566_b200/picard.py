@@ -22,8 +22,9 @@ from . import _lib
 def contraction_constant(G: float, c_min: float, L_D: float, delta: float, L_H: float,
                          m0: float, H_star: float, P_star: float) -> float:
     """q of Assumption 1 item 5 (Eq. contraction_const; R18 uses 2G/c_min):
-    q = (2G/c_min)·(2 L_D/δ)·(L_H/m0² + 2 H* P*/m0⁴)."""
-    return (2.0 * G / c_min) * (2.0 * L_D / delta) * (L_H / m0**2 + 2.0 * H_star * P_star / m0**4)
+    q = (2G/c_min)·(2 L_D/δ)·(L_H/m0² + 2 H* P*/m0⁴) — hjmc_contraction_constant."""
+    return float(_lib.load().hjmc_contraction_constant(G, c_min, L_D, delta, L_H, m0, H_star,
+                                                        P_star))
 
 
 @dataclass
@@ -41,14 +42,19 @@ class ContractionReport:
 
     @classmethod
     def from_differences(cls, d_sup, q_theory: float | None = None) -> "ContractionReport":
-        d = np.asarray(d_sup, dtype=np.float64)
-        with np.errstate(divide="ignore", invalid="ignore"):
-            q_hat = d[1:] / d[:-1] if d.size >= 2 else np.zeros(0)
-        apost = None
-        certified = q_theory is not None and 0.0 <= q_theory < 1.0
-        if certified:
-            apost = q_theory / (1.0 - q_theory) * d   # bound on ‖v^(k+1) − v*‖∞ from d_k
-        return cls(d, q_hat, q_theory, apost, certified)
+        """Marshals d_sup through hjmc_contraction_report (ratios and the a-posteriori bound
+        are computed in the library)."""
+        d = np.ascontiguousarray(d_sup, dtype=np.float64)
+        q_hat = np.zeros(max(d.size - 1, 0))
+        apost = np.zeros(d.size)
+        q = float(q_theory) if q_theory is not None else -1.0
+        rc = _lib.load().hjmc_contraction_report(
+            d.ctypes.data_as(C.c_void_p), d.size, q, q_hat.ctypes.data_as(C.c_void_p),
+            apost.ctypes.data_as(C.c_void_p))
+        if rc < 0:
+            raise _lib.HjmcError(1, "contraction_report")
+        certified = rc == 1
+        return cls(d, q_hat, q_theory, apost if certified else None, certified)
 
 
 def solve_adaptive(solver, x, tol: float, max_iter: int, qid_base: int = 0, qid=None,
