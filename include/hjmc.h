@@ -328,6 +328,33 @@ HJMC_API int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, 
 HJMC_API int hjmc_picard_decide(const double* partials, int32_t K, double tol, uint8_t* active,
                                 double* eps, double* dsup, int32_t* n_active);
 
+/* Algorithm 1 with its stopping test for a SHARDED slice, device-resident (no host round trip
+ * per iterate): the caller enqueues, on one stream, hjmc_picard_dev_begin once and then
+ * max_iter times { hjmc_picard_dev_pass; an all-reduce of `reduced` across the shards — rows 0–1
+ * summed, row 2 maxed (e.g. NCCL through torch.distributed, or nothing for one process);
+ * hjmc_picard_dev_decide } — the sequence can be captured into one CUDA graph.
+ *   dev_begin  — v^(0) = g, c^(0) = Γ(x, Dg) for every horizon, all horizons active, k = 0,
+ *                iters [K] = 0, eps / dsup [K][max_iter] = NaN (device outputs). x / qid /
+ *                drift must stay valid until the last call.
+ *   dev_pass   — one Φ pass of every still-active horizon (retired horizons' units exit at
+ *                once), v (dev [K][M], required), dv ([K][M][n]) and c ([K][M]) as
+ *                hjmc_picard_pass writes them, and reduced (dev double [3][K]) = this
+ *                handle's (Σ(v^(k+1)−v^(k))², Σ(v^(k))², max|v^(k+1)−v^(k)|) per horizon,
+ *                zeros for retired ones. No synchronisation, no allocation (capturable).
+ *   dev_decide — Algorithm 1 step 5 on the (all-reduced) reduced partials, the same
+ *                double expression as hjmc_picard_solve's decision kernel: records ε_j(k), the
+ *                sup-norm difference and the iterate count of every active horizon, retires it
+ *                when ε_j(k) < tol, advances k; a no-op past max_iter. Capturable.
+ * With one process (no all-reduce) the results equal hjmc_picard_solve bit for bit. */
+HJMC_API int hjmc_picard_dev_begin(hjmc_handle* h, const float* x, const uint32_t* qid,
+                                   uint32_t qid_base, int64_t M, const float* drift,
+                                   int32_t max_iter, int32_t* iters, double* eps, double* dsup,
+                                   void* stream);
+HJMC_API int hjmc_picard_dev_pass(hjmc_handle* h, float* v, float* dv, float* c, double* reduced,
+                                  void* stream);
+HJMC_API int hjmc_picard_dev_decide(hjmc_handle* h, const double* reduced, double tol,
+                                    int32_t* iters, double* eps, double* dsup, void* stream);
+
 /* Theorem 2's contraction constant (Eq. contraction_const; R18 reads 2G/c_min):
  *   q = (2G/c_min) · (2 L_D/δ) · (L_H/m0² + 2 H_star P_star / m0⁴).  Host-only, no handle. */
 HJMC_API double hjmc_contraction_constant(double G, double c_min, double L_D, double delta, double L_H,

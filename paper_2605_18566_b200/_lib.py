@@ -32,7 +32,8 @@ EXPORTS = [
     "hjmc_last_bad_query", "hjmc_last_error", "hjmc_residual_partials", "hjmc_version",
     "hjmc_pass_count", "hjmc_picard_begin", "hjmc_picard_pass", "hjmc_picard_solve",
     "hjmc_set_avoid", "hjmc_picard_decide", "hjmc_residual_eps", "hjmc_tube",
-    "hjmc_contraction_constant", "hjmc_contraction_report",
+    "hjmc_contraction_constant", "hjmc_contraction_report", "hjmc_picard_dev_begin",
+    "hjmc_picard_dev_pass", "hjmc_picard_dev_decide",
 ]
 
 
@@ -104,6 +105,9 @@ def load(path: str = LIB_PATH):
     L.hjmc_contraction_constant.argtypes = [dd] * 8
     L.hjmc_contraction_constant.restype = dd
     L.hjmc_contraction_report.argtypes = [vp, i64, dd, vp, vp]
+    L.hjmc_picard_dev_begin.argtypes = [vp, vp, vp, u32, i64, vp, C.c_int32, vp, vp, vp, vp]
+    L.hjmc_picard_dev_pass.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.hjmc_picard_dev_decide.argtypes = [vp, vp, dd, vp, vp, vp, vp]
     for name in EXPORTS:
         if not hasattr(L, name):
             raise RuntimeError(f"libhjmc.so lacks {name}")

@@ -71,6 +71,9 @@ struct hjmc_handle {
   cudaGraph_t pic_graph = nullptr;
   cudaGraphExec_t pic_exec = nullptr;
   std::vector<uintptr_t> pic_key;
+  // sharded device-resident Algorithm 1 (hjmc_picard_dev_*)
+  int pic_dev_max_iter = 0;
+  int pic_dev_blocks = 0;
 };
 
 namespace {
@@ -803,6 +806,127 @@ int hjmc_picard_pass(hjmc_handle* h, int32_t k, const uint8_t* active, float* v,
     o[2] = mx;
   }
   return sync_check_if_requested(h, s);
+}
+
+// Sharded device-resident Algorithm 1: the graph mode's kernels without the conditional node,
+// driven by the caller so a collective can sit between the residual and the decision.
+int hjmc_picard_dev_begin(hjmc_handle* h, const float* x, const uint32_t* qid, uint32_t qid_base,
+                          int64_t M, const float* drift, int32_t max_iter, int32_t* iters,
+                          double* eps, double* dsup, void* stream) {
+  NvtxRange nvtx_range("hjmc_picard_dev_begin");
+  int rc = ready(h);
+  if (rc) return rc;
+  if (M < 1 || !x) return fail(h, HJMC_EINVAL, "need M >= 1 and x");
+  if (M * (int64_t)h->cfg.K > 0x7FFFFFFFLL) return fail(h, HJMC_EINVAL, "M*K exceeds 2^31-1");
+  if (max_iter < 1 || !iters || !eps || !dsup)
+    return fail(h, HJMC_EINVAL, "need max_iter >= 1 and iters, eps, dsup");
+  if (!h->cfg.crn && max_iter > 256) return fail(h, HJMC_EINVAL, "max_iter must be <= 256 without crn");
+  if ((rc = set_device(h))) return rc;
+  const int K = h->cfg.K;
+  const size_t KM = (size_t)M * (size_t)K;
+  const int blocks = (int)std::min<int64_t>(148, (M + 255) / 256);
+  const size_t need = (size_t)K * (size_t)blocks * 3;
+  if (KM > h->cstate_cap) {
+    if (h->d_cstate) cudaFree(h->d_cstate);
+    h->d_cstate = nullptr;
+    h->cstate_cap = 0;
+    if (cudaMalloc((void**)&h->d_cstate, KM * sizeof(double)) != cudaSuccess)
+      return fail(h, HJMC_ENOMEM, "picard state allocation failed");
+    h->cstate_cap = KM;
+  }
+  if ((rc = ensure(h, &h->d_vprev, &h->vprev_cap, KM))) return rc;
+  if (need > h->partial_cap) {
+    if (h->d_partial) cudaFree(h->d_partial);
+    h->d_partial = nullptr;
+    h->partial_cap = 0;
+    if (cudaMalloc((void**)&h->d_partial, need * sizeof(double)) != cudaSuccess)
+      return fail(h, HJMC_ENOMEM, "picard partials allocation failed");
+    h->partial_cap = need;
+  }
+  if (!h->d_pstate && cudaMalloc((void**)&h->d_pstate, (2 * 65536 + 1) * sizeof(int)) != cudaSuccess)
+    return fail(h, HJMC_ENOMEM, "picard state allocation failed");
+  h->pic_x = x;
+  h->pic_qid = qid;
+  h->pic_qid_base = qid_base;
+  h->pic_M = M;
+  h->pic_drift = drift;
+  h->pic_dev_max_iter = max_iter;
+  h->pic_dev_blocks = blocks;
+  PicardInitParams ip{};
+  ip.x = x;
+  ip.M = M;
+  ip.K = K;
+  ip.c_state = h->d_cstate;
+  ip.v_prev = h->d_vprev;
+  ip.gp.delta_eff = delta_eff(h->cfg);
+  ip.gp.m0 = h->cfg.m0;
+  ip.gp.c_min = h->cfg.c_min;
+  ip.gp.c_max = h->cfg.c_max;
+  ip.sp = h->sp;
+  ip.tp = h->tp;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = h->ks.picard_init(ip, s);
+  if (e == cudaSuccess) e = launch_picard_solve_init(h->d_pstate, K, iters, eps, dsup, max_iter, s);
+  return e == cudaSuccess ? HJMC_OK : cuda_fail(h, e, "picard dev init launch");
+}
+
+int hjmc_picard_dev_pass(hjmc_handle* h, float* v, float* dv, float* c, double* reduced,
+                         void* stream) {
+  NvtxRange nvtx_range("hjmc_picard_dev_pass");
+  int rc = ready(h);
+  if (rc) return rc;
+  if (h->pic_M < 1 || h->pic_dev_max_iter < 1)
+    return fail(h, HJMC_EINVAL, "hjmc_picard_dev_begin has not been called");
+  if (!v || !reduced) return fail(h, HJMC_EINVAL, "v and reduced are required");
+  if ((rc = set_device(h))) return rc;
+  const int K = h->cfg.K;
+  const int64_t M = h->pic_M;
+  int* st = h->d_pstate;
+  SolveParams p;
+  fill_common(h, &p);
+  p.x = h->pic_x;
+  p.drift = h->pic_drift;
+  p.qid = h->pic_qid;
+  p.qid_base = h->pic_qid_base;
+  p.M = M;
+  p.K = K;
+  p.Kp = 1;
+  p.T = (double)h->cfg.T;
+  p.mode = kModePass;
+  p.v = v;
+  p.dv = dv;
+  p.c_out = c;
+  p.c_state = h->d_cstate;
+  p.active_j = st;
+  p.n_active = K;
+  p.active_mask = st + K;
+  p.kiter_dev = st + 2 * K;
+  p.kiter = 0;
+  p.skip_stationary = 0;
+  p.reuse_passes = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = h->ks.solve(p, M * (int64_t)K, s);
+  if (e == cudaSuccess)
+    e = launch_picard_residual(v, h->d_vprev, M, st, K, h->d_partial, h->pic_dev_blocks, s);
+  if (e == cudaSuccess)
+    e = launch_picard_blocksum(h->d_partial, K, h->pic_dev_blocks, st + K, reduced, s);
+  return e == cudaSuccess ? HJMC_OK : cuda_fail(h, e, "picard dev pass launch");
+}
+
+int hjmc_picard_dev_decide(hjmc_handle* h, const double* reduced, double tol, int32_t* iters,
+                           double* eps, double* dsup, void* stream) {
+  NvtxRange nvtx_range("hjmc_picard_dev_decide");
+  int rc = ready(h);
+  if (rc) return rc;
+  if (h->pic_dev_max_iter < 1) return fail(h, HJMC_EINVAL, "hjmc_picard_dev_begin has not been called");
+  if (!reduced || !iters || !eps || !dsup || !(tol >= 0.0))
+    return fail(h, HJMC_EINVAL, "need reduced, iters, eps, dsup and tol >= 0");
+  if ((rc = set_device(h))) return rc;
+  const int K = h->cfg.K;
+  int* st = h->d_pstate;
+  cudaError_t e = launch_picard_decide_reduced(reduced, K, tol, h->pic_dev_max_iter, st + K,
+                                               st + 2 * K, iters, eps, dsup, (cudaStream_t)stream);
+  return e == cudaSuccess ? HJMC_OK : cuda_fail(h, e, "picard dev decide launch");
 }
 
 int hjmc_eval_target(hjmc_handle* h, const float* x, int64_t M, float* g, float* dg, void* stream) {

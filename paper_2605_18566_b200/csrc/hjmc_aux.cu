@@ -135,6 +135,50 @@ __global__ void picard_decide_kernel(const double* __restrict__ partial, int K, 
   cudaGraphSetConditional(cond, (any && k + 1 < max_iter) ? 1u : 0u);
 }
 
+// Sharded device-resident Algorithm 1 (hjmc_picard_dev_pass / _decide): the per-rank block
+// partials summed per horizon in the decision kernel's fixed block order, laid out [3][K]
+// (Σ(v^(k+1)−v^(k))², Σ(v^(k))², max|v^(k+1)−v^(k)|) so a caller can all-reduce rows 0–1 (sum)
+// and row 2 (max) in place; zeros for retired horizons.
+__global__ void picard_blocksum_kernel(const double* __restrict__ partial, int K, int blocks,
+                                       const int* __restrict__ mask, double* __restrict__ red) {
+  if (threadIdx.x != 0) return;
+  for (int j = 0; j < K; ++j) {
+    double num = 0.0, den = 0.0, mx = 0.0;
+    if (mask[j]) {
+      for (int b = 0; b < blocks; ++b) {
+        const double* q = partial + ((size_t)j * blocks + b) * 3;
+        num += q[0];
+        den += q[1];
+        mx = fmax(mx, q[2]);
+      }
+    }
+    red[j] = num;
+    red[K + j] = den;
+    red[2 * K + j] = mx;
+  }
+}
+
+// Algorithm 1's stopping test on reduced [3][K] partials: the same double expression as
+// picard_decide_kernel; records ε, the sup-norm difference and the iterate count of every
+// active horizon, retires it when ε < tol, advances k. Without a conditional node the caller
+// runs max_iter of these; once nothing is active the passes early-exit and this only counts.
+__global__ void picard_decide_reduced_kernel(const double* __restrict__ red, int K, double tol,
+                                             int max_iter, int* mask, int* kiter, int* iters,
+                                             double* eps, double* dsup) {
+  if (threadIdx.x != 0) return;
+  const int k = *kiter;
+  if (k >= max_iter) return;
+  for (int j = 0; j < K; ++j) {
+    if (!mask[j]) continue;
+    const double e = sqrt(red[j] / fmax(red[K + j], 1e-300));
+    eps[(size_t)j * max_iter + k] = e;
+    dsup[(size_t)j * max_iter + k] = red[2 * K + j];
+    iters[j] = k + 1;
+    if (e < tol) mask[j] = 0;
+  }
+  *kiter = k + 1;
+}
+
 __global__ void picard_solve_init_kernel(int* state, int K, int32_t* iters, double* eps,
                                          double* dsup, int max_iter) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -156,6 +200,20 @@ cudaError_t launch_picard_solve_init(int* state, int K, int32_t* iters, double* 
                                      double* dsup, int max_iter, cudaStream_t s) {
   const int n = std::max(K, K * max_iter);
   picard_solve_init_kernel<<<(n + 255) / 256, 256, 0, s>>>(state, K, iters, eps, dsup, max_iter);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_picard_blocksum(const double* partial, int K, int blocks, const int* mask,
+                                   double* reduced, cudaStream_t s) {
+  picard_blocksum_kernel<<<1, 32, 0, s>>>(partial, K, blocks, mask, reduced);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_picard_decide_reduced(const double* reduced, int K, double tol, int max_iter,
+                                         int* mask, int* kiter, int* iters, double* eps,
+                                         double* dsup, cudaStream_t s) {
+  picard_decide_reduced_kernel<<<1, 32, 0, s>>>(reduced, K, tol, max_iter, mask, kiter, iters,
+                                                eps, dsup);
   return cudaGetLastError();
 }
 

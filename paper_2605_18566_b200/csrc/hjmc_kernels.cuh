@@ -117,6 +117,13 @@ cudaError_t launch_picard_residual(const float* v, float* v_prev, int64_t M, con
 cudaError_t launch_picard_decide(const double* partial, int K, int blocks, double tol,
                                  int max_iter, int* mask, int* kiter, int* iters, double* eps,
                                  double* dsup, cudaGraphConditionalHandle cond, cudaStream_t s);
+// Sharded device-resident Algorithm 1: per-horizon block sums → reduced [3][K] (zeros for retired
+// horizons), and the stopping test on (all-reduced) reduced partials (no conditional node).
+cudaError_t launch_picard_blocksum(const double* partial, int K, int blocks, const int* mask,
+                                   double* reduced, cudaStream_t s);
+cudaError_t launch_picard_decide_reduced(const double* reduced, int K, double tol, int max_iter,
+                                         int* mask, int* kiter, int* iters, double* eps,
+                                         double* dsup, cudaStream_t s);
 // Loop state for hjmc_picard_solve: horizons 1..K, all active, k = 0, iters = 0, NaN histories.
 cudaError_t launch_picard_solve_init(int* state, int K, int32_t* iters, double* eps,
                                      double* dsup, int max_iter, cudaStream_t s);

@@ -174,3 +174,62 @@ def solve_adaptive_device(solver, x, tol: float, max_iter: int, qid_base: int = 
     conv = np.array([it[j] > 0 and eps_h[j, it[j] - 1] < tol for j in range(K)])
     return {"v": v, "dv": dv, "c": c, "iters": it, "eps": eps_h, "d_sup": dsup.cpu().numpy(),
             "tube": tube, "converged": conv}
+
+
+def solve_adaptive_resident(solver, x, tol: float, max_iter: int, qid_base: int = 0, qid=None,
+                            drift=None, group=None, graph: bool = False, want_dv: bool = True):
+    """Algorithm 1 with its stopping test for a sharded slice, device-resident: every iterate is
+    {hjmc_picard_dev_pass → all-reduce of the [3][K] partials on the stream (NCCL through
+    torch.distributed when `group` is given: rows 0–1 summed, row 2 maxed) →
+    hjmc_picard_dev_decide}, enqueued max_iter times with no host round trip (retired horizons'
+    passes exit at once); graph=True captures the whole loop, collectives included, into one
+    CUDA graph and replays it. With one process it equals solve_adaptive_device bit for bit.
+    Returns the dict of solve_adaptive_device (v, dv, c, iters, eps, d_sup, tube, converged)."""
+    t = solver.torch
+    cfg = solver.cfg
+    x = solver._as_query(x)
+    M, K, n = x.shape[0], cfg.K, cfg.n
+    q = solver._as_dev(qid, t.int32) if qid is not None else None
+    b = solver._as_dev(drift) if drift is not None else None
+    dev = solver.device
+    v = t.empty((K, M), device=dev)
+    dv = t.empty((K, M, n), device=dev) if want_dv else None
+    c = t.empty((K, M), device=dev)
+    iters = t.zeros(K, dtype=t.int32, device=dev)
+    eps = t.empty((K, max_iter), dtype=t.float64, device=dev)
+    dsup = t.empty((K, max_iter), dtype=t.float64, device=dev)
+    red = t.empty((3, K), dtype=t.float64, device=dev)
+    tube = t.empty(M, device=dev)
+    L = solver.L
+    ptr = lambda a: C.c_void_p(a.data_ptr()) if a is not None else None
+    solver._check(L.hjmc_picard_dev_begin(solver.h, ptr(x), ptr(q), qid_base, M, ptr(b),
+                                          int(max_iter), ptr(iters), ptr(eps), ptr(dsup),
+                                          solver._stream()))
+
+    def body():
+        import torch.distributed as dist
+
+        stream = solver._stream()
+        for _ in range(max_iter):
+            solver._check(L.hjmc_picard_dev_pass(solver.h, ptr(v), ptr(dv), ptr(c), ptr(red),
+                                                 stream))
+            if group is not None:
+                dist.all_reduce(red[:2], op=dist.ReduceOp.SUM, group=group)
+                dist.all_reduce(red[2], op=dist.ReduceOp.MAX, group=group)
+            solver._check(L.hjmc_picard_dev_decide(solver.h, ptr(red), float(tol), ptr(iters),
+                                                   ptr(eps), ptr(dsup), stream))
+
+    if graph:
+        t.cuda.synchronize(dev)
+        g = t.cuda.CUDAGraph()
+        with t.cuda.graph(g):
+            body()
+        g.replay()
+    else:
+        body()
+    solver._check(L.hjmc_tube(solver.h, ptr(x), M, ptr(v), ptr(tube), solver._stream()))
+    eps_h = eps.cpu().numpy()
+    it = iters.cpu().numpy().astype(np.int64)
+    conv = np.array([it[j] > 0 and eps_h[j, it[j] - 1] < tol for j in range(K)])
+    return {"v": v, "dv": dv, "c": c, "iters": it, "eps": eps_h, "d_sup": dsup.cpu().numpy(),
+            "tube": tube, "converged": conv}
