@@ -444,10 +444,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": cfg,
-        "s_per_slice": step_s * per_slice_q / (Mtot / len(preset.slices)),
-        "s_per_slice_basis": (f"extrapolated: step time × {per_slice_q} / {Mtot // len(preset.slices)}"
-                              " queries per slice (per-query work is fixed)"
-                              if Mtot < preset.M else "measured: one slice per step"),
+        "s_per_slice": step_s * per_slice_q / Mtot,
+        "s_per_slice_basis": (f"extrapolated: step time × {per_slice_q} queries per slice / {Mtot} "
+                              "queries per step (per-query work is fixed)"
+                              if Mtot != per_slice_q else "measured: one slice per step"),
         "kernel_ms_per_step": kern_avg_ms,
         "gpu_launches": 2 * args.steps,
         "roofline": roof,

@@ -28,6 +28,10 @@ VARIANTS = {
     "single3": ["-DHJMC_LG_DUAL=0", "-DHJMC_MINB=3"],
     "dual4": ["-DHJMC_LG_DUAL=1", "-DHJMC_MINB=4"],
     "dual3": ["-DHJMC_LG_DUAL=1", "-DHJMC_MINB=3"],
+    # generic per-thread kernel (C4, n = 15): more samples in flight at 2 CTAs/SM
+    "mb2": ["-DHJMC_MINB=2"],
+    "mb2u4": ["-DHJMC_MINB=2", "-DHJMC_UNROLL=4"],
+    "mb3u4": ["-DHJMC_MINB=3", "-DHJMC_UNROLL=4"],
 }
 # Also measured this round and removed from the source (same queries, same box): a software-
 # pipelined dual loop (the next pair's Philox words generated in the body that transforms this
