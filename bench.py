@@ -219,6 +219,25 @@ def run_reference(args):
     return 0
 
 
+def _measured_full_slice(preset):
+    """A complete 2-D slice of the workload measured (not extrapolated) by
+    tools/config_bench.py --full-slice, if profiles/ holds one for this preset (context beside
+    the extrapolated s_per_slice; not re-measured by this run)."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_full_slice*.jsonl")), reverse=True):
+        with open(path) as fh:
+            for line in fh:
+                try:
+                    r = json.loads(line)
+                except ValueError:
+                    continue
+                if r.get("config") == preset.name and r.get("measured_full_slice"):
+                    return {"s": r["ms"] / 1000.0, "s_exact_shortcuts": r["fastpath"]["ms"] / 1000.0,
+                            "source": os.path.relpath(path, ROOT)}
+    return None
+
+
 # ---- our arm --------------------------------------------------------------------------------
 GATHER_KEYS = ("v", "dv", "c", "tube", "vhist")
 
@@ -448,6 +467,7 @@ def run_ours(args):
         "s_per_slice_basis": (f"extrapolated: step time × {per_slice_q} queries per slice / {Mtot} "
                               "queries per step (per-query work is fixed)"
                               if Mtot != per_slice_q else "measured: one slice per step"),
+        "s_per_slice_measured": _measured_full_slice(preset),
         "kernel_ms_per_step": kern_avg_ms,
         "gpu_launches": 2 * args.steps,
         "roofline": roof,
