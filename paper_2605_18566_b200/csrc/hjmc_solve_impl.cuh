@@ -259,11 +259,15 @@ __device__ __forceinline__ void cta_reduce(SolveSmem<NDIM, NT>& sm, float S, flo
 // Targets whose core is a min over (x, y) pairs of 3-coordinate blocks: the K-pair union and the
 // paper's pursuit-min, where every lane also needs the evader's sampled position — it
 // lives in one lane and reaches the others by two shuffles.
+#ifndef HJMC_NO_LANE_GROUPS
+#define HJMC_NO_LANE_GROUPS 0   // build variant: the per-thread layout at n = 37–48 too
+#endif
 template <class Tgt, int NDIM>
 struct UseLaneGroups {
   static constexpr bool kPursuit = std::is_same<Tgt, PursuitMin<NDIM>>::value;
   static constexpr bool value =
-      (std::is_same<Tgt, PairUnion<NDIM>>::value || kPursuit) && NDIM >= 37 && NDIM <= 48;
+      (std::is_same<Tgt, PairUnion<NDIM>>::value || kPursuit) && NDIM >= 37 && NDIM <= 48 &&
+      !HJMC_NO_LANE_GROUPS;
 };
 
 #ifndef HJMC_LG_LANES
@@ -275,7 +279,11 @@ constexpr int kLgLanes = HJMC_LG_LANES;
 #ifndef HJMC_LG_DUAL
 #define HJMC_LG_DUAL 1
 #endif
+#ifndef HJMC_LG_DUAL_UNROLL
+#define HJMC_LG_DUAL_UNROLL 1
+#endif
 constexpr bool kLgDual = HJMC_LG_DUAL != 0;  // two samples per lane-group trip (lg_pass)
+constexpr int kLgDualUnroll = HJMC_LG_DUAL_UNROLL;
 
 constexpr int kLgSpan = 48 / kLgLanes;
 static_assert(kLgLanes == 2 || kLgLanes == 4, "lane groups of 2 or 4");
@@ -394,6 +402,7 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
     // The min is exact and each weight is formed from the same fp32 values by the same MUFU
     // ops, and S, Mb accumulate w_t then w_{t+1} as the one-sample loop does: bit-identical.
     const bool lo = l < 2;
+#pragma unroll(kLgDualUnroll)
     for (; t0 + 1 < full; t0 += 2) {
       float z0[kLgSpan], z1[kLgSpan];
       draw(t0 * kStride + slot, z0);

@@ -28,6 +28,9 @@ VARIANTS = {
     "single3": ["-DHJMC_LG_DUAL=0", "-DHJMC_MINB=3"],
     "dual4": ["-DHJMC_LG_DUAL=1", "-DHJMC_MINB=4"],
     "dual3": ["-DHJMC_LG_DUAL=1", "-DHJMC_MINB=3"],
+    "nolg2": ["-DHJMC_NO_LANE_GROUPS=1", "-DHJMC_MINB=2"],
+    "du2": ["-DHJMC_LG_DUAL_UNROLL=2"],
+    "du4": ["-DHJMC_LG_DUAL_UNROLL=4"],
     # generic per-thread kernel (C4, n = 15): more samples in flight at 2 CTAs/SM
     "mb2": ["-DHJMC_MINB=2"],
     "mb2u4": ["-DHJMC_MINB=2", "-DHJMC_UNROLL=4"],
