@@ -41,7 +41,11 @@ VARIANTS = {
 # pair) 4908 ms vs 4417 ms; a prototype draw layout with 6 normals per Philox block (3 Box–Muller
 # pairs from 128 bits: 30 % fewer IMAD.WIDE) 4259 ms, pipelined 4201 ms — 4–5 %, too little to
 # change the frozen sampler contract (R19) and every golden fixture for: the kernel is bound by
-# the MUFU/issue co-limit, not by the wide multiplies alone.
+# the MUFU/issue co-limit, not by the wide multiplies alone. Later the same day:
+# Philox's three c0-only wide multiplies computed once per lane pair and exchanged by four xor-2
+# shuffles (bit-identical, 4 IMAD.WIDE fewer per lane per two samples) 4531 vs 4450 ms; the
+# dual loop unrolled x2 / x4 4504 / 4619 vs 4454 ms; 2-lane groups 4473 vs 4455 ms; the
+# per-thread layout at 128 registers (spilling) 4873 vs 4458 ms.
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
