@@ -402,6 +402,11 @@ def run_ours(args):
                       f"{', 4-lane groups' if lane else ''}> (+ tube epilogue, <0.1%)",
             "kernel_ms_avg": kern_avg_ms, "units_per_launch": int(count * preset.K),
             "evals_per_launch": int(evals_step_rank)}
+    # every pipe's share of its own peak at the minimal per-eval counts (the metric names the
+    # FP32/MUFU peak; the binding pipe above is the one with the largest demand)
+    evals_per_s_kernel = evals_step_rank / (kern_avg_ms / 1000.0)
+    roof["by_pipe"] = {k: rl["ops"][k] * evals_per_s_kernel / (rates[k] * RL.NSM * RL.F_MAX_MHZ * 1e6)
+                       for k in ("imul", "mufu", "fp32", "alu", "issue")}
     if clk and clk.get("sm_mhz"):
         roof["frac_at_measured_clock"] = roof["frac"] * 1965.0 / clk["sm_mhz"]
     # the query / result streams (north_star: "achieved HBM GB/s"): per unit the kernel reads x
