@@ -423,15 +423,22 @@ def run_ours(args):
                    "peak_gbps": hbm_peak,
                    "frac": (hbm_gbps / hbm_peak) if hbm_peak else None,
                    "note": "no sample touches HBM; the streams are queries and per-iterate results"}
-    mix_file = os.path.join(ROOT, "profiles", "r1_mix_ceiling.json")
-    if preset.name == "c2_dubins_n3" and os.path.exists(mix_file):
-        with open(mix_file) as fh:
-            mix = json.load(fh)["mixes"]["full_c2_mix"]["evals_per_clk_per_sm"]
-        f_hz = (clk["sm_mhz"] if clk and clk.get("sm_mhz") else RL.F_MAX_MHZ) * 1e6
-        per_clk = evals_step_rank / (kern_avg_ms / 1000.0) / (RL.NSM * f_hz)
-        roof["mix_ceiling"] = {"evals_per_clk_per_sm": mix, "kernel_evals_per_clk_per_sm": per_clk,
-                               "frac": per_clk / mix,
-                               "source": "profiles/r1_mix_ceiling.json (synthetic same-mix kernel)"}
+    # context for the fraction: the measured throughput ceiling of this kernel's own instruction
+    # mix (a synthetic kernel with the same per-eval mix and no memory)
+    f_hz = (clk["sm_mhz"] if clk and clk.get("sm_mhz") else RL.F_MAX_MHZ) * 1e6
+    per_clk = evals_step_rank / (kern_avg_ms / 1000.0) / (RL.NSM * f_hz)
+    mixes = {"c2_dubins_n3": ("r1_mix_ceiling.json", "full_c2_mix", "evals_per_clk_per_sm", 1.0),
+             "c5_dubins15pairs_n45": ("r2_mix_ceiling_c5.json", "full_mix_2samples_2cta",
+                                      "lane_samples_per_clk_per_sm", 4.0)}
+    if preset.name in mixes:
+        fname, key, field, lanes = mixes[preset.name]
+        mix_file = os.path.join(ROOT, "profiles", fname)
+        if os.path.exists(mix_file):
+            with open(mix_file) as fh:
+                mix = json.load(fh)["mixes"][key][field] / lanes
+            roof["mix_ceiling"] = {"evals_per_clk_per_sm": mix,
+                                   "kernel_evals_per_clk_per_sm": per_clk, "frac": per_clk / mix,
+                                   "source": f"profiles/{fname} (synthetic same-mix kernel)"}
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(traffic_file):
         with open(traffic_file) as fh:
