@@ -812,3 +812,22 @@ def test_picard_resident_sharded_driver_equals_graph():
             for k in ("v", "dv", "c", "tube"):
                 assert torch.equal(a[k], b[k]), k
         assert len(set(a["iters"])) >= 1
+
+
+@pytest.mark.parametrize("N", [3000, 40000, 70000, 1500])   # warp / 4-warp / CTA groups; n = 45 lanes
+def test_repeated_launches_bit_identical(N):
+    """Race check by repetition (compute-sanitizer is closed on this pool): the same solve
+    relaunched with the units' placement in CTAs shifted — a leading block of extra queries
+    moves every unit to another CTA slot and named-barrier group — must give bit-identical
+    results for the queries in common, for the warp, 4-warp (bar.sync 1 + g, 128) and CTA
+    groups and for the lane-group kernel (N = 1500 at n = 45)."""
+    p = I.C2.with_(N=N, K=2, Kp=3) if N != 1500 else I.C5.with_(N=N, K=2, Kp=2)
+    s = Solver(SolverConfig.from_preset(p))
+    x_all = I.queries(p)[:260]
+    ref = s.solve_slice(x_all[5:], qid_base=5)
+    for shift in (0, 1, 2, 3, 5):
+        for _ in range(2):
+            out = s.solve_slice(x_all[5 - shift:], qid_base=5 - shift)
+            for k in ("v", "dv", "c", "tube"):
+                assert torch.equal(out[k][shift:], ref[k]), (N, shift, k)
+            assert torch.equal(out["vhist"][:, :, shift:], ref["vhist"]), (N, shift)
