@@ -821,7 +821,7 @@ def test_repeated_launches_bit_identical(N):
     moves every unit to another CTA slot and named-barrier group — must give bit-identical
     results for the queries in common, for the warp, 4-warp (bar.sync 1 + g, 128) and CTA
     groups and for the lane-group kernel (N = 1500 at n = 45)."""
-    p = I.C2.with_(N=N, K=2, Kp=3) if N != 1500 else I.C5.with_(N=N, K=2, Kp=2)
+    p = I.C2.with_(N=N, K=3, Kp=3) if N != 1500 else I.C5.with_(N=N, K=3, Kp=2)
     s = Solver(SolverConfig.from_preset(p))
     x_all = I.queries(p)[:260]
     ref = s.solve_slice(x_all[5:], qid_base=5)
