@@ -156,9 +156,9 @@ def oracle_pass_sample(preset, ids, x_all, count: int, offset: int = 0, nthreads
 
 
 def pass_seconds(preset) -> float:
-    """Host-core seconds of one oracle Φ pass (two sweeps over N samples; measured ≈ 1e-7 s
-    per sample·coordinate on these hosts)."""
-    return preset.N * max(preset.n, 3) * 1.0e-7
+    """Host-core seconds of one oracle Φ pass (two sweeps over N samples), modelled from the
+    GPU box's host: 15.6 ms at C2 (n = 3, N = 2^16), 2.06 s at C5 (n = 45, N = 2^20)."""
+    return preset.N * (1.0e-7 + 3.5e-8 * preset.n)
 
 
 def auto_passes(preset, seconds: float) -> int:
@@ -452,7 +452,7 @@ def run_ours(args):
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cnt = args.cpu_sample or auto_passes(preset, 15.0)
+        cnt = args.cpu_sample or auto_passes(preset, 20.0)
         v, dt, used, cores = oracle_pass_sample(preset, ids, x_all, cnt)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{used} Φ passes of the workload (the first Picard pass of sampled "
