@@ -72,8 +72,75 @@ __device__ __forceinline__ void mul_wide(uint32_t a, uint32_t m, uint32_t& hi, u
       : "r"(a), "r"(m));
 }
 
+// ---- the high word of a Philox product on the FP64 pipe -----------------------------------------
+// IMAD.WIDE.U32 occupies the FMA-heavy pipe for 4 cycles per warp, and that pipe is one of the
+// three co-limits of the sample loop. The same product can be split: the low word
+// by IMAD (2 cycles, FMA-heavy) and the high word by ONE DFMA on the separate FP64 pipe, exactly.
+// Carry a 32-bit word c as the double whose bit pattern is {lo = c, hi = 0x43300000}, i.e.
+// a = 2^52 + c. With b = M·2^-32 and K = 2^52 − 2^20·M (both exact: M and 2^32 − M are 32-bit
+// integers scaled by powers of two),
+//   fma.rm(a, b, K) = 2^52 + c·M·2^-32 rounded down = 2^52 + floor(c·M / 2^32),
+// because c·M·2^-32 < 2^32 keeps the sum in [2^52, 2^53) where one ulp is 1. So the result's low
+// word IS mulhi(c, M) and its high word is again 0x43300000 — the pattern the next round's input
+// needs, since the round's XOR rewrites only the low word. Exact integer arithmetic: bit-identical
+// to IMAD.WIDE by construction.
+// Which of the 20 products take the FP64 path: bit 2r = round r's c0·M0 product, bit 2r + 1 =
+// round r's c2·M1 product. 0 = IMAD.WIDE everywhere.
+#ifndef HJMC_PHILOX_DFMA_MASK
+#define HJMC_PHILOX_DFMA_MASK 0u
+#endif
+constexpr uint64_t kPairHi = 0x4330000000000000ull;  // {lo = c, hi = 0x43300000} = 2^52 + c
+
+template <uint32_t kM>
+__device__ __forceinline__ uint64_t mulhi_dfma(uint64_t pair) {
+  constexpr double kB = (double)kM * (1.0 / 4294967296.0);
+  constexpr double kK = 4503599627370496.0 - 1048576.0 * (double)kM;  // 2^52 − 2^20·M
+  double r;
+  asm("fma.rm.f64 %0, %1, %2, %3;" : "=d"(r) : "d"(__longlong_as_double((long long)pair)),
+      "d"(kB), "d"(kK));
+  return (uint64_t)__double_as_longlong(r);
+}
+
+template <uint32_t kMask>
+__device__ __forceinline__ uint4 philox4x32_10_mixed(uint32_t c0, uint32_t c1, uint32_t c2,
+                                                     uint32_t c3, const RoundKeys& rk) {
+  constexpr uint32_t kMul0 = 0xD2511F53u, kMul1 = 0xCD9E8D57u;
+  // p0 / p2: c0 / c2 carried as {word, 0x43300000}; the XOR below touches only the low word
+  uint64_t p0 = kPairHi | c0, p2 = kPairHi | c2;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const bool d0 = (kMask >> (2 * r)) & 1u, d1 = (kMask >> (2 * r + 1)) & 1u;
+    const uint32_t w0 = (uint32_t)p0, w2 = (uint32_t)p2;
+    uint64_t h0, h1;  // {mulhi, 0x43300000}
+    uint32_t lo0, lo1;
+    if (d0) {
+      h0 = mulhi_dfma<kMul0>(p0);
+      lo0 = w0 * kMul0;
+    } else {
+      uint32_t hi;
+      mul_wide(w0, kMul0, hi, lo0);
+      h0 = kPairHi | hi;
+    }
+    if (d1) {
+      h1 = mulhi_dfma<kMul1>(p2);
+      lo1 = w2 * kMul1;
+    } else {
+      uint32_t hi;
+      mul_wide(w2, kMul1, hi, lo1);
+      h1 = kPairHi | hi;
+    }
+    p0 = h1 ^ (uint64_t)(c1 ^ rk.k0[r]);
+    p2 = h0 ^ (uint64_t)(c3 ^ rk.k1[r]);
+    c1 = lo1;
+    c3 = lo0;
+  }
+  return make_uint4((uint32_t)p0, c1, (uint32_t)p2, c3);
+}
+
 __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
                                                const RoundKeys& rk) {
+  if constexpr (HJMC_PHILOX_DFMA_MASK != 0u)
+    return philox4x32_10_mixed<HJMC_PHILOX_DFMA_MASK>(c0, c1, c2, c3, rk);
   constexpr uint32_t kMul0 = 0xD2511F53u, kMul1 = 0xCD9E8D57u;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {

@@ -35,6 +35,14 @@ VARIANTS = {
     "mb2": ["-DHJMC_MINB=2"],
     "mb2u4": ["-DHJMC_MINB=2", "-DHJMC_UNROLL=4"],
     "mb3u4": ["-DHJMC_MINB=3", "-DHJMC_UNROLL=4"],
+    # Philox products' high words on the FP64 pipe (DFMA.RM, hjmc_rng.cuh), by product mask.
+    # Bit-identical on C2-C5 but slower everywhere (C5 1,184 queries: base 4462 ms, df5 4643,
+    # dfHi 4836, dfLo 4969, dfA 5310; profiles/r2_philox_dfma_variants.jsonl)
+    "dfA": ["-DHJMC_PHILOX_DFMA_MASK=0xFFFFFu"],
+    "df5": ["-DHJMC_PHILOX_DFMA_MASK=0x55555u"],
+    "dfA5": ["-DHJMC_PHILOX_DFMA_MASK=0xAAAAAu"],
+    "dfLo": ["-DHJMC_PHILOX_DFMA_MASK=0x003FFu"],
+    "dfHi": ["-DHJMC_PHILOX_DFMA_MASK=0xFFC00u"],
 }
 # Also measured this round and removed from the source (same queries, same box): a software-
 # pipelined dual loop (the next pair's Philox words generated in the body that transforms this

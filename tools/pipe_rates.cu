@@ -78,6 +78,43 @@ DEFINE_BENCH(b_imad_hi, uint32_t, (uint32_t)p0 + threadIdx.x + c,
 // logic (ALU pipe): 3-input XOR chains across neighbouring chains
 DEFINE_BENCH(b_lop3, uint32_t, (uint32_t)p0 + threadIdx.x * 7u + c,
              v[c] = v[c] ^ v[(c + 3) % kChains] ^ (p1 + c))
+// FP64 (DFMA) and the exact Philox high word on the FP64 pipe (hjmc_rng.cuh mulhi_dfma):
+// {c, 0x43300000} = 2^52 + c; fma.rm(2^52 + c, M·2^-32, 2^52 − 2^20·M) = 2^52 + mulhi(c, M)
+#define DEFINE_DBENCH(NAME, INIT, BODY)                                                   \
+  __global__ void NAME(double* out, Stamp* st, double p0, double p1, double p2) {         \
+    double v[kChains];                                                                    \
+    for (int c = 0; c < kChains; ++c) v[c] = INIT;                                        \
+    __syncthreads();                                                                      \
+    long long t0 = clock64();                                                             \
+    for (int it = 0; it < kIters; ++it) {                                                 \
+      _Pragma("unroll") for (int c = 0; c < kChains; ++c) { BODY; }                       \
+    }                                                                                     \
+    __syncthreads();                                                                      \
+    long long t1 = clock64();                                                             \
+    double acc = v[0];                                                                    \
+    for (int c = 1; c < kChains; ++c) acc = acc + v[c];                                   \
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;                                     \
+    if (threadIdx.x == 0) st[blockIdx.x] = Stamp{t0, t1, smid()};                         \
+  }
+DEFINE_DBENCH(b_dfma, p0 + threadIdx.x * 1e-9 + c, v[c] = fma(v[c], p1, p2))
+__device__ __forceinline__ uint32_t mulhi_dfma_pr(uint32_t c) {
+  constexpr uint32_t kM = 0xD2511F53u;
+  const double b = (double)kM * (1.0 / 4294967296.0), k = 4503599627370496.0 - 1048576.0 * (double)kM;
+  double a = __hiloint2double(0x43300000, (int)c), r;
+  asm volatile("fma.rm.f64 %0, %1, %2, %3;" : "=d"(r) : "d"(a), "d"(b), "d"(k));
+  return (uint32_t)__double2loint(r);
+}
+// body: mulhi on the FP64 pipe + the low word by IMAD + one LOP3 (the IMAD.WIDE body's work)
+DEFINE_BENCH(b_dfma_mulhi, uint32_t, (uint32_t)p0 + threadIdx.x + c,
+             { uint32_t hi = mulhi_dfma_pr(v[c]); v[c] = (v[c] * 0xD2511F53u) ^ hi; })
+// body: mulhi on the FP64 pipe + one LOP3 (no low word): the FP64 pipe's own rate for the trick
+DEFINE_BENCH(b_dfma_mulhi_only, uint32_t, (uint32_t)p0 + threadIdx.x + c,
+             v[c] = mulhi_dfma_pr(v[c]) ^ (p1 + c))
+__global__ void check_dfma_mulhi(const uint32_t* in, unsigned* bad, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && mulhi_dfma_pr(in[i]) != __umulhi(in[i], 0xD2511F53u)) atomicAdd(bad, 1u);
+}
+
 // MUFU (XU pipe)
 DEFINE_FBENCH(b_ex2, p0 + threadIdx.x * 1e-6f + c * 1e-3f, v[c] = ex2a(-v[c]))
 DEFINE_FBENCH(b_sqrt, p0 + 2.0f + threadIdx.x * 1e-3f + c, v[c] = sqrta(v[c]))
@@ -128,16 +165,39 @@ int main() {
   r.push_back({"imad_lo", "imad_lo", run<uint32_t>(b_imad_lo, 1u, 0x9E3779B9u, 0u, nsm)});
   r.push_back({"imad_hi (+lop3)", "imad_hi", run<uint32_t>(b_imad_hi, 1u, 0x9E3779B9u, 0u, nsm)});
   r.push_back({"lop3", "alu", run<uint32_t>(b_lop3, 1u, 0x9E3779B9u, 0u, nsm)});
+  r.push_back({"dfma", "fp64", run<double>(b_dfma, 1.0, 0.999999, 1e-9, nsm)});
+  r.push_back({"dfma_mulhi + imad_lo (+lop3)", "fp64+imad", run<uint32_t>(b_dfma_mulhi, 1u, 0u, 0u, nsm)});
+  r.push_back({"dfma_mulhi (+lop3)", "fp64", run<uint32_t>(b_dfma_mulhi_only, 1u, 0x9E3779B9u, 0u, nsm)});
   r.push_back({"mufu_ex2", "mufu", run<float>(b_ex2, 0.5f, 0.f, 0.f, nsm)});
   r.push_back({"mufu_sqrt", "mufu_sqrt", run<float>(b_sqrt, 0.f, 0.f, 0.f, nsm)});
   r.push_back({"mufu_lg2 (+fadd)", "mufu_lg2", run<float>(b_lg2, 0.f, 2.0f, 0.f, nsm)});
   r.push_back({"mufu_cos (+fmul.rz)", "mufu_cos", run<float>(b_cos, 0.5f, 0.f, 0.f, nsm)});
+  // exactness of the FP64 high word on 2^24 inputs (edge words + a multiplicative sweep)
+  unsigned long long bad_total = 0;
+  {
+    const int n = 1 << 24;
+    std::vector<uint32_t> h(n);
+    uint32_t x = 0x12345678u;
+    for (int i = 0; i < n; ++i) { x = x * 1664525u + 1013904223u; h[i] = x; }
+    const uint32_t edges[] = {0u, 1u, 2u, 0x7FFFFFFFu, 0x80000000u, 0xFFFFFFFEu, 0xFFFFFFFFu};
+    for (int i = 0; i < 7; ++i) h[i] = edges[i];
+    uint32_t* d; unsigned* b;
+    cudaMalloc(&d, sizeof(uint32_t) * n); cudaMalloc(&b, sizeof(unsigned));
+    cudaMemcpy(d, h.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice);
+    cudaMemset(b, 0, sizeof(unsigned));
+    check_dfma_mulhi<<<(n + 255) / 256, 256>>>(d, b, n);
+    unsigned hb = 0;
+    cudaMemcpy(&hb, b, sizeof(unsigned), cudaMemcpyDeviceToHost);
+    bad_total = hb;
+    cudaFree(d); cudaFree(b);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     fprintf(stderr, "CUDA error %s\n", cudaGetErrorString(e));
     return 1;
   }
   printf("{\n  \"device_sms\": %d, \"clock_rate_khz\": %d,\n", nsm, clk);
+  printf("  \"dfma_mulhi_mismatches_of_2^24\": %llu,\n", bad_total);
   printf("  \"method\": \"per-SM clock64 window over 4 CTAs x 256 threads x 8 chains; median over SMs\",\n");
   printf("  \"raw\": {\n");
   for (size_t i = 0; i < r.size(); ++i)
