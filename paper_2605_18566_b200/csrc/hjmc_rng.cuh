@@ -185,6 +185,18 @@ __device__ __forceinline__ void box_muller_hat(uint32_t w_r, uint32_t w_a, float
   if (kNeedSin) zs = rh * sin_approx(th);
 }
 
+// The same transform left in polar form: ẑ_cos = rh·c, ẑ_sin = rh·s. The lane-group kernel keeps
+// (rh, c, s) and never forms the products: the sample position comes from one FFMA per
+// coordinate in σ-scaled coordinates, the moments from the pair's w·rh (hjmc_solve_impl.cuh).
+__device__ __forceinline__ void box_muller_polar(uint32_t w_r, uint32_t w_a, float& rh, float& c,
+                                                 float& s) {
+  constexpr float kTwoPi = 6.2831853071795865f;
+  rh = sqrt_approx(fabsf(lg2_approx(unif_open(w_r))));
+  const float th = kTwoPi * mantissa_float(w_a);
+  c = cos_approx(th);
+  s = sin_approx(th);
+}
+
 // Counter word 1 for quad b: b | kw << 8 | jw << 16.
 __device__ __forceinline__ uint32_t ctr_word1(uint32_t b, uint32_t kw, uint32_t jw) {
   return b | (kw << 8) | (jw << 16);

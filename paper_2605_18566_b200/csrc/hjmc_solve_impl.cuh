@@ -294,23 +294,33 @@ struct LgSpec {
   float A, B, S, S1, Mb[kLgSpan];
 };
 
+// σ-scaled coordinates (round 2). The pass works on y/σ' (σ' = σC, the transform scale):
+// x' = x/σ' once per unit, so a sample coordinate is x' + ẑ = x' + rh·trig — ONE FFMA from the
+// polar Box–Muller output (rh, cos, sin), with no rh·trig product; the moments take the pair's
+// w·rh (one FMUL per pair instead of one per coordinate). The pair-union core is homogeneous,
+// core(y) = σ'·core(y/σ'), so the caller passes A' = fl(A·σ') and the epilogue undoes A'/σ'
+// (kernel: A_eff). Per lane and sample this removes 6 FP32 multiplies of ~210 instructions.
+// x' carries one extra rounding, |x|·2^-24 absolute in position (the unscaled fma rounds once
+// at |y|), far inside R20. Coordinates past n get x' = 1e18 (a sentinel whose |pos|² = 2e36
+// never wins the min), so the pair-union partial min needs no per-lane guard.
 template <int NDIM, int NT, bool kMaxMode, bool kPursuit = false, bool kSpec = false>
 __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float tau, float sigma_s,
                                         float A, float B, uint32_t w1base, uint32_t qid,
                                         float& S, float (&Mb)[kLgSpan], float& amax,
                                         LgSpec* sp = nullptr) {
-  constexpr int kBlocks = kLgSpan / 4, kTriples = kLgSpan / 3;
+  constexpr int kBlocks = kLgSpan / 4, kTriples = kLgSpan / 3, kPairs = kLgSpan / 2;
   const int lane = threadIdx.x & 31, l = lane & (kLgLanes - 1);
   const uint32_t slot = (threadIdx.x >> 5) * (32 / kLgLanes) + (lane / kLgLanes);  // sample slot
   constexpr uint32_t kStride = NT / kLgLanes;
-  float xb[kLgSpan];
+  float xb[kLgSpan];  // x' = x / σ'
 #pragma unroll
   for (int c = 0; c < kLgSpan; ++c) {
     const int d = kLgSpan * l + c;
-    float xv = 0.f;
+    float xv = kPursuit ? 0.f : 1.0e18f;
     if (d < NDIM) {
       xv = P.x[m * NDIM + d];
       if (P.drift) xv = __fadd_rn(xv, __fmul_rn(P.drift[m * NDIM + d], tau));
+      xv = __fdiv_rn(xv, sigma_s);
     }
     xb[c] = xv;
   }
@@ -319,43 +329,55 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
 #pragma unroll
   for (int c = 0; c < kLgSpan; ++c) Mb[c] = 0.f;
   const uint32_t N = P.N;
-  // this lane's 12 normals of sample i (its Philox blocks kBlocks·l .. kBlocks·l + kBlocks − 1)
-  auto draw = [&](uint32_t i, float (&z)[kLgSpan]) {
+  // this lane's share of sample i in polar form: ẑ_c = r[c/2]·t[c] (its Philox blocks
+  // kBlocks·l .. kBlocks·l + kBlocks − 1; pair p = normals 2p, 2p + 1)
+  struct Draw {
+    float t[kLgSpan], r[kPairs];
+  };
+  auto draw = [&](uint32_t i, Draw& z) {
 #pragma unroll
     for (int qd = 0; qd < kBlocks; ++qd) {
       const uint4 w = philox4x32_10(i, w1base | (uint32_t)(kBlocks * l + qd), qid, P.tag, P.rk);
-      box_muller_hat<true>(w.x, w.y, z[4 * qd], z[4 * qd + 1]);
-      box_muller_hat<true>(w.z, w.w, z[4 * qd + 2], z[4 * qd + 3]);
+      box_muller_polar(w.x, w.y, z.r[2 * qd], z.t[4 * qd], z.t[4 * qd + 1]);
+      box_muller_polar(w.z, w.w, z.r[2 * qd + 1], z.t[4 * qd + 2], z.t[4 * qd + 3]);
     }
   };
+  auto coord = [&](const Draw& z, int c) { return fmaf(z.r[c / 2], z.t[c], xb[c]); };
 
-
-  // min over this lane's (x, y) pairs of |pos|² (pursuit: |pursuer − evader|²)
-  auto partial_min = [&](const float (&z)[kLgSpan]) -> float {
+  // min over this lane's (x, y) pairs of |pos'|² (pursuit: |pursuer − evader|²), pos' = y/σ'
+  auto partial_min = [&](const Draw& z) -> float {
     float best = 3.0e38f;
     if constexpr (kPursuit) {
       // the evader (last agent, coordinates kE, kE + 1) is owned by lane kE / kLgSpan
       constexpr int kE = NDIM - 3, kLaneE = kE / kLgSpan, kCE = kE % kLgSpan;
       const int src = (lane & ~(kLgLanes - 1)) | kLaneE;
-      const float ex = __shfl_sync(0xffffffffu, fmaf(sigma_s, z[kCE], xb[kCE]), src);
-      const float ey = __shfl_sync(0xffffffffu, fmaf(sigma_s, z[kCE + 1], xb[kCE + 1]), src);
+      const float ex = __shfl_sync(0xffffffffu, coord(z, kCE), src);
+      const float ey = __shfl_sync(0xffffffffu, coord(z, kCE + 1), src);
 #pragma unroll
       for (int pq = 0; pq < kTriples; ++pq) {
-        const float a = fmaf(sigma_s, z[3 * pq], xb[3 * pq]) - ex;
-        const float b = fmaf(sigma_s, z[3 * pq + 1], xb[3 * pq + 1]) - ey;
+        const float a = coord(z, 3 * pq) - ex;
+        const float b = coord(z, 3 * pq + 1) - ey;
         const float r2 = fmaf(a, a, b * b);
         best = (kLgSpan * l + 3 * pq < kE) ? fminf(best, r2) : best;   // pursuers only
       }
     } else {
 #pragma unroll
       for (int pq = 0; pq < kTriples; ++pq) {
-        const float a = fmaf(sigma_s, z[3 * pq], xb[3 * pq]);
-        const float b = fmaf(sigma_s, z[3 * pq + 1], xb[3 * pq + 1]);
-        const float r2 = fmaf(a, a, b * b);
-        best = (kLgSpan * l + 3 * pq + 1 < NDIM) ? fminf(best, r2) : best;
+        const float a = coord(z, 3 * pq);
+        const float b = coord(z, 3 * pq + 1);
+        best = fminf(best, fmaf(a, a, b * b));  // coordinates past n: the 1e18 sentinel
       }
     }
     return best;
+  };
+  // Mb[c] += w·ẑ_c as (w·rh_p)·trig_c
+  auto moments = [&](float (&acc)[kLgSpan], float w, const Draw& z) {
+#pragma unroll
+    for (int p = 0; p < kPairs; ++p) {
+      const float wr = w * z.r[p];
+      acc[2 * p] = fmaf(wr, z.t[2 * p], acc[2 * p]);
+      acc[2 * p + 1] = fmaf(wr, z.t[2 * p + 1], acc[2 * p + 1]);
+    }
   };
   // One sample per lane group per trip; trips where every slot's sample exists run without
   // the i < N guard (C5: N = 2^20, all of them), the ragged last trip with it.
@@ -367,7 +389,7 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
   // uses the same split, so a speculative pass still equals a real one bit for bit.
   float S1 = 0.f;
   auto trip = [&](uint32_t i, bool guard, bool odd) {
-    float z[kLgSpan];
+    Draw z;
     draw(i, z);
     float best = partial_min(z);
 #pragma unroll
@@ -380,14 +402,12 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
         const float wt = ex2_approx(fmaf(A, core, B));
         if (odd) S1 += wt;
         else S += wt;
-#pragma unroll
-        for (int c = 0; c < kLgSpan; ++c) Mb[c] = fmaf(wt, z[c], Mb[c]);
+        moments(Mb, wt, z);
         if constexpr (kSpec) {
           const float w2 = ex2_approx(fmaf(sp->A, core, sp->B));
           if (odd) sp->S1 += w2;
           else sp->S += w2;
-#pragma unroll
-          for (int c = 0; c < kLgSpan; ++c) sp->Mb[c] = fmaf(w2, z[c], sp->Mb[c]);
+          moments(sp->Mb, w2, z);
         }
       }
     }
@@ -404,7 +424,7 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
     const bool lo = l < 2;
 #pragma unroll(kLgDualUnroll)
     for (; t0 + 1 < full; t0 += 2) {
-      float z0[kLgSpan], z1[kLgSpan];
+      Draw z0, z1;
       draw(t0 * kStride + slot, z0);
       draw((t0 + 1) * kStride + slot, z1);
       const float b0 = partial_min(z0), b1 = partial_min(z1);
@@ -416,11 +436,9 @@ __device__ __forceinline__ void lg_pass(const SolveParams& P, int64_t m, float t
       const float wo = __shfl_xor_sync(0xffffffffu, wm, 2);
       const float w0 = lo ? wm : wo, w1 = lo ? wo : wm;
       S += w0;                                                     // t0 even
-#pragma unroll
-      for (int c = 0; c < kLgSpan; ++c) Mb[c] = fmaf(w0, z0[c], Mb[c]);
+      moments(Mb, w0, z0);
       S1 += w1;                                                    // t0 + 1 odd
-#pragma unroll
-      for (int c = 0; c < kLgSpan; ++c) Mb[c] = fmaf(w1, z1[c], Mb[c]);
+      moments(Mb, w1, z1);
     }
   }
 #pragma unroll(kLgUnroll)
@@ -468,7 +486,7 @@ __device__ __forceinline__ void lg_reduce(SolveSmem<NDIM, NT>& sm, float S, floa
 template <class Tgt, int NDIM>
 __device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tgt, int64_t m, int j,
                                              int k, uint32_t id, double c, double sigma_d,
-                                             float A, float B, float core_ref, const double* sum,
+                                             double A, float B, float core_ref, const double* sum,
                                              const double* dshift, bool* done) {
   const double A_d = -c * kLog2e;
   const double Ssum = sum[0];
@@ -477,7 +495,7 @@ __device__ __noinline__ double pass_epilogue(const SolveParams& P, const Tgt& tg
     for (int d = 0; d < NDIM; ++d) tilt_log2 -= 0.5 * dshift[d] * dshift[d] * kLog2e;
   // log2 of (1/N) Σ exp(−c g_i)·LR_i: undo the shift B and the fp32 rounding of A
   const double log2mean = log2(Ssum) - log2((double)P.N) - (double)B + A_d * (double)tgt.off +
-                          (A_d - (double)A) * (double)core_ref + tilt_log2;
+                          (A_d - A) * (double)core_ref + tilt_log2;
   const double v = -(kLn2 / c) * log2mean;                           // Cor. logsumexp
   double dv[NDIM];
   bool finite = isfinite(v);
@@ -578,9 +596,14 @@ __device__ __noinline__ double unit_prologue(const SolveParams& P, const Tgt& tg
 #define HJMC_MINB 0
 #endif
 template <int NDIM, bool kLG, bool kSpec = false>
+#ifndef HJMC_LG_SPEC_MINB
+#define HJMC_LG_SPEC_MINB 2
+#endif
 constexpr int min_blocks() {
   if (HJMC_MINB > 0) return HJMC_MINB;
-  if (kLG && kSpec) return kLgLanes == 4 ? 3 : 2;  // + 12 speculative moments per lane
+  // + 12 speculative moments per lane; with the σ-scaled pass (polar draws, 18 live floats per
+  // sample) 2 CTAs/SM beat 3 (C5 fastpath 479 vs 502 ms; 3 CTAs spill inside the loop)
+  if (kLG && kSpec) return kLgLanes == 4 ? HJMC_LG_SPEC_MINB : 2;
   // two samples in flight (kLgDual) need 128 registers: 2 CTAs/SM, measured 1.9 % faster on C5
   // than one sample at 4 CTAs/SM; 2-lane groups hold 24 + 24 + 16 floats
   if (kLG) return (kLgLanes == 4 && !kLgDual) ? 4 : 2;
@@ -676,6 +699,10 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
                                                 : P.ktag;
     const uint32_t w1base = (kw << 8) | (jw << 16);
     const float A = opaque((float)(-c * kLog2e));
+    // lane-group passes run in σ-scaled coordinates (lg_pass): A' = fl(A·σ'), and the epilogue
+    // takes the effective A'/σ' in place of A
+    const float A_lg = kLG ? opaque(A * sigma_s) : A;
+    const double A_eff = kLG ? (double)A_lg / (double)sigma_s : (double)A;
     // Proposal centre (R28): plain → x + bτ; Laplace → μ = x + bτ − cσ²·Dg(x + bτ) (fp32, every
     // thread computes the same values in double); tz = log2-domain tilt per ẑ coordinate.
     // The lane-group kernel (plain proposal only) has thread 0 derive B and core_ref from the
@@ -745,8 +772,9 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
         if constexpr (kSpec) {
           if (do_spec) {
             LgSpec sp;
-            sp.A = opaque((float)(-c_spec * kLog2e));
-            if (tid == 0) sm.lg_B2 = -sp.A * tgt.core_lower(sm.xs, sigma);  // as a pass at c_spec
+            const float A_spec = opaque((float)(-c_spec * kLog2e));
+            sp.A = opaque(A_spec * sigma_s);  // exactly the A' a pass at c_spec would use
+            if (tid == 0) sm.lg_B2 = -A_spec * tgt.core_lower(sm.xs, sigma);  // as a pass at c_spec
             __syncthreads();
             sp.B = opaque(sm.lg_B2);
             sp.S = 0.f;
@@ -754,7 +782,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
 #pragma unroll
             for (int c2 = 0; c2 < kLgSpan; ++c2) sp.Mb[c2] = 0.f;
             lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit, true>(
-                P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax, &sp);
+                P, m, (float)tau, sigma_s, A_lg, B, w1base, id, S, Mb, amax, &sp);
             lg_reduce<NDIM, NT>(sm, S, Mb);
             lg_reduce<NDIM, NT>(sm, sp.S, sp.Mb, sm.sum2);
             B_spec = sp.B;
@@ -762,8 +790,9 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
           }
         }
         if (plain_lg) {
-          lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A,
-                                                                       B, w1base, id, S, Mb, amax);
+          lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s,
+                                                                       A_lg, B, w1base, id, S, Mb,
+                                                                       amax);
           lg_reduce<NDIM, NT>(sm, S, Mb);
         }
       } else {
@@ -798,7 +827,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
         float amax_t;
         if constexpr (kLG) {
           float S, Mb[kLgSpan];
-          lg_pass<NDIM, NT, true, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, amax_t);
+          lg_pass<NDIM, NT, true, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A_lg, B, w1base, id, S, Mb, amax_t);
         } else {
           amax_t = mc_max_exponent<Tgt, NDIM, GS>(tgt, ctr, sigma_s, A, P.N, P.antithetic, w1base,
                                                   id, P.tag, P.rk, tz, tid);
@@ -815,7 +844,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
         B = -sm.shift;
         if constexpr (kLG) {
           float S, Mb[kLgSpan], am;
-          lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A, B, w1base, id, S, Mb, am);
+          lg_pass<NDIM, NT, false, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A_lg, B, w1base, id, S, Mb, am);
           lg_reduce<NDIM, NT>(sm, S, Mb);
         } else {
           float S, Mz[NDIM];
@@ -854,7 +883,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
       if constexpr (kProp) {
         for (int d = 0; d < NDIM; ++d) dsh[d] = ((double)ctr[d] - (double)xs[d]) / sigma_d;
       }
-      sm.c_next = pass_epilogue<Tgt, NDIM>(P, tgt, m, j, k, id, c, sigma_d, A, B, core_ref, sums,
+      sm.c_next = pass_epilogue<Tgt, NDIM>(P, tgt, m, j, k, id, c, sigma_d, A_eff, B, core_ref, sums,
                                            kProp ? dsh : nullptr, &done);
       sm.shift = done ? 1.f : 0.f;
     }

@@ -33,6 +33,9 @@ def test_c5_counts_by_hand():
     ops = RL.op_counts(45, "pair_union")
     assert ops["imul"] == 183
     assert ops["mufu"] == 93
+    # FP32: per pair u = F − (1 − 2⁻²⁴) and w·r̂ (σ-scaled coordinates: no r̂·cos, r̂·sin), 2·23;
+    # per sample 15 × (2 positions + FMUL + FFMA for |pos|²) + A·core + B + S += w + 45 moments
+    assert ops["fp32"] == 2 * 23 + 15 * 4 + 1 + 1 + 45
 
 
 def test_binding_pipes_with_measured_rates():

@@ -38,6 +38,8 @@ VARIANTS = {
     # Philox products' high words on the FP64 pipe (DFMA.RM, hjmc_rng.cuh), by product mask.
     # Bit-identical on C2-C5 but slower everywhere (C5 1,184 queries: base 4462 ms, df5 4643,
     # dfHi 4836, dfLo 4969, dfA 5310; profiles/r2_philox_dfma_variants.jsonl)
+    # lane-group speculative kernel at 2 CTAs/SM (128 registers) instead of 3
+    "spec2": ["-DHJMC_LG_SPEC_MINB=2"],
     "dfA": ["-DHJMC_PHILOX_DFMA_MASK=0xFFFFFu"],
     "df5": ["-DHJMC_PHILOX_DFMA_MASK=0x55555u"],
     "dfA5": ["-DHJMC_PHILOX_DFMA_MASK=0xAAAAAu"],

@@ -1,7 +1,8 @@
 """A/B timing of libhjmc build variants on the benchmark's C5 workload (a prefix of
 inputs.bench_ids, full N, K, Kp), with a bit-identity check of every output against the first
-variant. Usage: python tools/lg_variant_bench.py [count] [config] — variants from
-variants/libhjmc_*.so plus the in-tree library ("base")."""
+variant. Usage: python tools/lg_variant_bench.py [count] [config] [solver-flags-json] — variants
+from variants/libhjmc_*.so plus the in-tree library ("base"); flags e.g.
+'{"skip_stationary": 1, "reuse_passes": 1, "speculate": 1}' time the exact shortcuts."""
 import glob
 import json
 import os
@@ -16,10 +17,10 @@ sys.path.insert(0, "{root}")
 from paper_2605_18566_b200 import _lib, inputs as I
 _lib.load("{lib}")
 from paper_2605_18566_b200.solver import Solver, SolverConfig
-p = I.BY_INDEX[{cfg}]
+p = I.BY_INDEX[{cfg}] if isinstance({cfg}, int) else I.PRESETS[{cfg}]
 ids = I.bench_ids(p)
 ids = ids[np.linspace(0, len(ids) - 1, min({count}, len(ids))).round().astype(int)]
-s = Solver(SolverConfig.from_preset(p))
+s = Solver(SolverConfig.from_preset(p, **{flags}))
 x = torch.from_numpy(np.ascontiguousarray(I.queries(p)[ids])).cuda()
 q = torch.from_numpy(ids.astype(np.int32)).cuda()
 out = s.alloc_result(x.shape[0])
@@ -37,13 +38,15 @@ print(json.dumps({{"ms": ms, "evals_per_s": len(ids) * p.N * p.K * p.Kp / (ms / 
 
 if __name__ == "__main__":
     count = int(sys.argv[1]) if len(sys.argv) > 1 else 1184
-    cfg = int(sys.argv[2].lstrip("c")) if len(sys.argv) > 2 else 5
+    arg = sys.argv[2] if len(sys.argv) > 2 else "5"
+    cfg = int(arg.lstrip("c")) if arg.lstrip("c").isdigit() else repr(arg)
+    flags = json.loads(sys.argv[3]) if len(sys.argv) > 3 else {}
     libs = [os.path.join(ROOT, "paper_2605_18566_b200", "libhjmc.so")]
     libs += sorted(glob.glob(os.path.join(ROOT, "variants", "libhjmc_*.so")))
     for lib in libs:
-        code = CHILD.format(root=ROOT, lib=lib, cfg=cfg, count=count, reps=2)
+        code = CHILD.format(root=ROOT, lib=lib, cfg=cfg, count=count, reps=2, flags=repr(flags))
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
         line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-400:]
         name = "base" if "variants" not in lib else os.path.basename(lib)[7:-3]
-        print(json.dumps({"variant": name, "config": f"c{cfg}", "queries": count,
+        print(json.dumps({"variant": name, "config": f"c{cfg}" if isinstance(cfg, int) else arg, "queries": count, "flags": flags,
                           "result": line}), flush=True)
