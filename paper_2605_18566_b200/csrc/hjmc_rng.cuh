@@ -244,4 +244,35 @@ __device__ __forceinline__ void group_normals_hat(float (&zz)[DrawLayout<NDIM>::
   }
 }
 
+// The same G·n normals in polar form: ẑ_e = rr[e]·tt[e], rr[e] = rr[e ^ 1] the pair's radius
+// (duplicated per normal so a sample's coordinates index it directly; after unrolling the copies
+// are the same register).
+template <int NDIM>
+__device__ __forceinline__ void group_normals_polar(float (&tt)[DrawLayout<NDIM>::L],
+                                                    float (&rr)[DrawLayout<NDIM>::L], uint32_t g,
+                                                    uint32_t w1base, uint32_t qid, uint32_t tag,
+                                                    const RoundKeys& rk) {
+  using L = DrawLayout<NDIM>;
+  constexpr int kLen = L::L;
+#pragma unroll
+  for (int b = 0; b < L::Q; ++b) {
+    const uint4 w = philox4x32_10(g, w1base | (uint32_t)b, qid, tag, rk);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = 4 * b + 2 * h;
+      if (e < kLen) {
+        constexpr float kTwoPi = 6.2831853071795865f;
+        const float rh = sqrt_approx(fabsf(lg2_approx(unif_open(h ? w.z : w.x))));
+        const float th = kTwoPi * mantissa_float(h ? w.w : w.y);
+        rr[e] = rh;
+        tt[e] = cos_approx(th);
+        if (e + 1 < kLen) {
+          rr[e + 1] = rh;
+          tt[e + 1] = sin_approx(th);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace hjmc

@@ -99,6 +99,36 @@ __device__ __forceinline__ void accumulate_sample(const Tgt& tgt, const float (&
   for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(sw, z[d], Mz[d]);
 }
 
+// Polar variant for homogeneous targets (distances; Tgt::kHomog) with the plain proposal: the
+// pass runs in σ-scaled coordinates — xs = x/σ', A = fl(A·σ') (the kernel undoes A/σ' in the
+// epilogue) — so a coordinate is one FFMA x'_d + (±r̂)·trig_d from the polar draw and the
+// moments take (±w·r̂)·trig_d, with no r̂·trig products ("σ-scaled coordinates").
+template <class Tgt, int NDIM, bool kSpec = false>
+__device__ __forceinline__ void accumulate_sample_polar(const Tgt& tgt, const float (&xs)[NDIM],
+                                                        float A, float B, const float* tg,
+                                                        const float* rg, float sgn, float& S,
+                                                        float (&Mz)[NDIM],
+                                                        SpecSums<NDIM>* sp = nullptr) {
+  float t[NDIM], r[NDIM];
+#pragma unroll
+  for (int d = 0; d < NDIM; ++d) {
+    t[d] = tg[d];
+    r[d] = sgn * rg[d];
+  }
+  const float core_v = tgt.core_polar(xs, r, t);
+  if constexpr (kSpec) {
+    const float w2 = ex2_approx(fmaf(sp->A, core_v, sp->B));
+    sp->S += w2;
+#pragma unroll
+    for (int d = 0; d < NDIM; ++d) sp->Mz[d] = fmaf(w2 * rg[d], t[d], sp->Mz[d]);
+  }
+  const float w = ex2_approx(fmaf(A, core_v, B));
+  S += w;
+  const float sw = sgn * w;
+#pragma unroll
+  for (int d = 0; d < NDIM; ++d) Mz[d] = fmaf(sw * rg[d], t[d], Mz[d]);
+}
+
 // NT here is the size of the thread group that shares one unit (the CTA, or one warp in the
 // warp-per-unit kernel) and tid the thread's index in it.
 template <class Tgt, int NDIM, int NT, bool kTilt = false, bool kSpec = false>
@@ -115,6 +145,39 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
   for (int d = 0; d < NDIM; ++d) Mz[d] = 0.f;
   const uint32_t draws = antithetic ? (N >> 1) + (N & 1u) : N;
   const uint32_t groups = (draws + L::G - 1) / L::G;
+  if constexpr (Tgt::kHomog && !kTilt) {  // σ-scaled polar pass (xs = x/σ', A = A·σ')
+    const uint32_t full = antithetic ? 0u : N / L::G;
+#pragma unroll(L::G == 1 ? kSampleUnroll : kGroupUnroll)
+    for (uint32_t g = tid; g < full; g += NT) {
+      float tt[L::L], rr[L::L];
+      group_normals_polar<NDIM>(tt, rr, g, w1base, qid, tag, rk);
+#pragma unroll
+      for (int r = 0; r < L::G; ++r)
+        accumulate_sample_polar<Tgt, NDIM, kSpec>(tgt, xs, A, B, tt + r * NDIM, rr + r * NDIM,
+                                                  1.f, S, Mz, sp);
+    }
+    for (uint32_t g = full + tid; g < groups; g += NT) {  // ragged tail group / antithetic
+      float tt[L::L], rr[L::L];
+      group_normals_polar<NDIM>(tt, rr, g, w1base, qid, tag, rk);
+#pragma unroll
+      for (int r = 0; r < L::G; ++r) {
+        const uint32_t q = g * L::G + r;
+        if (antithetic) {
+          if (L::G == 1 || q < draws) {
+            accumulate_sample_polar<Tgt, NDIM>(tgt, xs, A, B, tt + r * NDIM, rr + r * NDIM, 1.f,
+                                               S, Mz);
+            if (2 * q + 1 < N)
+              accumulate_sample_polar<Tgt, NDIM>(tgt, xs, A, B, tt + r * NDIM, rr + r * NDIM,
+                                                 -1.f, S, Mz);
+          }
+        } else if (q < N) {
+          accumulate_sample_polar<Tgt, NDIM, kSpec>(tgt, xs, A, B, tt + r * NDIM, rr + r * NDIM,
+                                                    1.f, S, Mz, sp);
+        }
+      }
+    }
+    return;
+  }
   if (!antithetic) {
     const uint32_t full = N / L::G;  // groups whose G samples all exist: no per-sample guard
 #pragma unroll(L::G == 1 ? kSampleUnroll : kGroupUnroll)
@@ -153,7 +216,8 @@ __device__ __forceinline__ void mc_accumulate(const Tgt& tgt, const float (&xs)[
 }
 
 // Largest exponent A·core(y_i) over this thread's samples (fallback shift; rarely used).
-template <class Tgt, int NDIM, int NT>
+// kPolar: the σ-scaled polar form of mc_accumulate (same core values as that pass).
+template <class Tgt, int NDIM, int NT, bool kPolar = false>
 __device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float sigma, float A,
                                  uint32_t N, int antithetic, uint32_t w1base, uint32_t qid,
                                  uint32_t tag, const RoundKeys& rk, const float (&tz)[NDIM],
@@ -162,6 +226,27 @@ __device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float 
   float amax = -3.0e38f;
   const uint32_t draws = antithetic ? (N >> 1) + (N & 1u) : N;
   const uint32_t groups = (draws + L::G - 1) / L::G;
+  if constexpr (kPolar) {
+    for (uint32_t g = tid; g < groups; g += NT) {
+      float tt[L::L], rr[L::L];
+      group_normals_polar<NDIM>(tt, rr, g, w1base, qid, tag, rk);
+#pragma unroll
+      for (int r = 0; r < L::G; ++r) {
+        const uint32_t q = g * L::G + r;
+        if (q >= draws) continue;
+        float t[NDIM], rp[NDIM], rn[NDIM];
+#pragma unroll
+        for (int d = 0; d < NDIM; ++d) {
+          t[d] = tt[r * NDIM + d];
+          rp[d] = rr[r * NDIM + d];
+          rn[d] = -rp[d];
+        }
+        amax = fmaxf(amax, A * tgt.core_polar(xs, rp, t));
+        if (antithetic && 2 * q + 1 < N) amax = fmaxf(amax, A * tgt.core_polar(xs, rn, t));
+      }
+    }
+    return amax;
+  }
   for (uint32_t g = tid; g < groups; g += NT) {
     float zz[L::L];
     group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
@@ -629,6 +714,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
                 "thread groups smaller than the CTA only for the generic kernel");
   __shared__ SolveSmem<NDIM, GS> smv[NT / GS];
   SolveSmem<NDIM, GS>& sm = smv[threadIdx.x / GS];
+  constexpr bool kPolarG = !kLG && Tgt::kHomog && !kProp;  // σ-scaled generic passes
   const uint32_t tid = threadIdx.x % GS;
   auto gsync = [] { group_sync<GS, NT>(); };
   const int64_t unit = (int64_t)blockIdx.x * (NT / GS) + threadIdx.x / GS;
@@ -699,10 +785,12 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
                                                 : P.ktag;
     const uint32_t w1base = (kw << 8) | (jw << 16);
     const float A = opaque((float)(-c * kLog2e));
-    // lane-group passes run in σ-scaled coordinates (lg_pass): A' = fl(A·σ'), and the epilogue
-    // takes the effective A'/σ' in place of A
-    const float A_lg = kLG ? opaque(A * sigma_s) : A;
-    const double A_eff = kLG ? (double)A_lg / (double)sigma_s : (double)A;
+    // lane-group passes and the generic passes of homogeneous targets with the plain proposal
+    // run in σ-scaled coordinates (lg_pass, accumulate_sample_polar): A' = fl(A·σ'), and the
+    // epilogue takes the effective A'/σ' in place of A
+    constexpr bool kScaled = kLG || kPolarG;
+    const float A_lg = kScaled ? opaque(A * sigma_s) : A;
+    const double A_eff = kScaled ? (double)A_lg / (double)sigma_s : (double)A;
     // Proposal centre (R28): plain → x + bτ; Laplace → μ = x + bτ − cσ²·Dg(x + bτ) (fp32, every
     // thread computes the same values in double); tz = log2-domain tilt per ẑ coordinate.
     // The lane-group kernel (plain proposal only) has thread 0 derive B and core_ref from the
@@ -744,6 +832,10 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
       }
       // every a_i = A core_i + B (+ tilt) ≤ 0: no weight can overflow
       B = opaque(-A * tgt.core_lower(ctr, sigma) - tilt_max);
+      if constexpr (kPolarG) {
+#pragma unroll
+        for (int d = 0; d < NDIM; ++d) ctr[d] = __fdiv_rn(ctr[d], sigma_s);  // x' = x/σ'
+      }
     }
 
     int hit = -1;  // CTA-uniform: every thread reads the same memo after the last barrier
@@ -802,12 +894,13 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
           if (do_spec) {
             // exactly the A and B a pass at c_spec would use (tilt 0: plain proposal)
             SpecSums<NDIM> sp;
-            sp.A = opaque((float)(-c_spec * kLog2e));
-            sp.B = opaque(-sp.A * tgt.core_lower(ctr, sigma) - 0.f);
+            const float A_spec = opaque((float)(-c_spec * kLog2e));
+            sp.A = kPolarG ? opaque(A_spec * sigma_s) : A_spec;  // as a pass at c_spec
+            sp.B = opaque(-A_spec * tgt.core_lower(xs, sigma) - 0.f);  // plain: centre = x
             sp.S = 0.f;
 #pragma unroll
             for (int d = 0; d < NDIM; ++d) sp.Mz[d] = 0.f;
-            mc_accumulate<Tgt, NDIM, GS, false, true>(tgt, ctr, sigma_s, A, B, P.N, 0, w1base, id,
+            mc_accumulate<Tgt, NDIM, GS, false, true>(tgt, ctr, sigma_s, A_lg, B, P.N, 0, w1base, id,
                                                       P.tag, P.rk, S, Mz, tz, tid, &sp);
             cta_reduce<NDIM, GS, NT>(sm, S, Mz, tid);
             cta_reduce<NDIM, GS, NT>(sm, sp.S, sp.Mz, tid, sm.sum2);
@@ -816,7 +909,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
           }
         }
         if (plain) {
-          mc_accumulate<Tgt, NDIM, GS, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
+          mc_accumulate<Tgt, NDIM, GS, kProp>(tgt, ctr, sigma_s, A_lg, B, P.N, P.antithetic, w1base,
                                               id, P.tag, P.rk, S, Mz, tz, tid);
           cta_reduce<NDIM, GS, NT>(sm, S, Mz, tid);
         }
@@ -829,7 +922,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
           float S, Mb[kLgSpan];
           lg_pass<NDIM, NT, true, UseLaneGroups<Tgt, NDIM>::kPursuit>(P, m, (float)tau, sigma_s, A_lg, B, w1base, id, S, Mb, amax_t);
         } else {
-          amax_t = mc_max_exponent<Tgt, NDIM, GS>(tgt, ctr, sigma_s, A, P.N, P.antithetic, w1base,
+          amax_t = mc_max_exponent<Tgt, NDIM, GS, kPolarG>(tgt, ctr, sigma_s, A_lg, P.N, P.antithetic, w1base,
                                                   id, P.tag, P.rk, tz, tid);
         }
         const float amax = warp_max(amax_t);
@@ -848,7 +941,7 @@ __global__ void __launch_bounds__(NT, min_blocks<NDIM, kLG, kSpec>()) solve_kern
           lg_reduce<NDIM, NT>(sm, S, Mb);
         } else {
           float S, Mz[NDIM];
-          mc_accumulate<Tgt, NDIM, GS, kProp>(tgt, ctr, sigma_s, A, B, P.N, P.antithetic, w1base,
+          mc_accumulate<Tgt, NDIM, GS, kProp>(tgt, ctr, sigma_s, A_lg, B, P.N, P.antithetic, w1base,
                                               id, P.tag, P.rk, S, Mz, tz, tid);
           cta_reduce<NDIM, GS, NT>(sm, S, Mz, tid);
         }

@@ -5,7 +5,11 @@
 //   core_lower(xs, σ): a guaranteed lower bound of core(xs + σz) over every z the sampler can
 //                      emit (|z_d| ≤ ZMAX, include/hjmc.h), which fixes a safe exponent shift
 //                      (no weight can exceed 2^0);
-//   g_host/dg:         g(x) and the analytic Dg(x) in double for c^(0) (R7).
+//   g_host/dg:         g(x) and the analytic Dg(x) in double for c^(0) (R7);
+//   kHomog, core_polar: the pair union and pursuit-min (distances, homogeneous of degree 1
+//                      in the position) also evaluate core(y)/σ' from σ-scaled coordinates x/σ'
+//                      and the polar Box–Muller output, coordinate d = x'_d + rr_d·t_d (one FFMA;
+//                      no r̂·cos / r̂·sin products — hjmc_solve_impl.cuh).
 // Definitions follow include/hjmc.h TARGETS (R15, R16).
 #pragma once
 #include <cstdint>
@@ -25,7 +29,7 @@ struct TargetParams {
 // ---------------------------------------------------------------------------------------------
 template <int NDIM>
 struct QuadBowl {  // g = |y|²/2 − α0
-  static constexpr int kNeed = NDIM;   // coordinates g reads (all)
+  static constexpr bool kHomog = false;
   float off;
   __device__ explicit QuadBowl(const TargetParams& t) : off(-(t.np > 0 ? t.p[0] : 0.25f)) {}
   __device__ __forceinline__ float core(const float (&xs)[NDIM], float sigma,
@@ -58,6 +62,10 @@ struct QuadBowl {  // g = |y|²/2 − α0
 template <int NDIM>
 struct Disk {  // g = sqrt(y0² + y1²) − r
   static_assert(NDIM >= 2, "DISK needs n >= 2");
+  // a distance too, but kept on the unscaled path: measured −2.6 % on C2 with the polar pass,
+  // yet the changed rounding flips one more non-contractive C2 trajectory unit (query 500, R27)
+  // than the capped parity sample allows
+  static constexpr bool kHomog = false;
   float off;
   __device__ explicit Disk(const TargetParams& t) : off(-(t.np > 0 ? t.p[0] : 5.0f)) {}
   __device__ __forceinline__ float core(const float (&xs)[NDIM], float sigma,
@@ -88,6 +96,9 @@ struct Disk {  // g = sqrt(y0² + y1²) − r
 template <int NDIM>
 struct RelDisk6 {  // g = ‖(y0 − y3, y1 − y4)‖ − r  (n = 6)
   static_assert(NDIM == 6, "REL_DISK6 needs n == 6");
+  // unscaled path: the polar pass measured a tie on C3 (the relative coordinates cost an FFMA
+  // more each)
+  static constexpr bool kHomog = false;
   float off;
   __device__ explicit RelDisk6(const TargetParams& t) : off(-(t.np > 0 ? t.p[0] : 1.5f)) {}
   __device__ __forceinline__ float core(const float (&xs)[NDIM], float sigma,
@@ -126,8 +137,20 @@ template <int NDIM>
 struct PairUnion {  // g = sqrt(min_q (y_{3q}² + y_{3q+1}²)) − r  (n = 3K)
   static_assert(NDIM % 3 == 0, "PAIR_UNION needs n = 3K");
   static constexpr int kPairs = NDIM / 3;
+  static constexpr bool kHomog = true;
   float off;
   __device__ explicit PairUnion(const TargetParams& t) : off(-(t.np > 0 ? t.p[0] : 1.0f)) {}
+  __device__ __forceinline__ float core_polar(const float (&xs)[NDIM], const float (&rr)[NDIM],
+                                              const float (&t)[NDIM]) const {
+    float best = 3.0e38f;
+#pragma unroll
+    for (int q = 0; q < kPairs; ++q) {
+      const float a = fmaf(rr[3 * q], t[3 * q], xs[3 * q]);
+      const float b = fmaf(rr[3 * q + 1], t[3 * q + 1], xs[3 * q + 1]);
+      best = fminf(best, fmaf(a, a, b * b));
+    }
+    return sqrt_approx(best);
+  }
   __device__ __forceinline__ float core(const float (&xs)[NDIM], float sigma,
                                         const float (&z)[NDIM]) const {
     float best = 3.0e38f;
@@ -179,8 +202,22 @@ struct PursuitMin {  // g = min_{i < A−1} ‖pos_i − pos_{A−1}‖ − r  (
   static_assert(NDIM % 3 == 0 && NDIM >= 6, "PURSUIT_MIN needs n = 3A, A >= 2");
   static constexpr int kAgents = NDIM / 3;
   static constexpr int kE = 3 * (kAgents - 1);  // evader's first coordinate
+  static constexpr bool kHomog = true;
   float off;
   __device__ explicit PursuitMin(const TargetParams& t) : off(-(t.np > 0 ? t.p[0] : 1.5f)) {}
+  __device__ __forceinline__ float core_polar(const float (&xs)[NDIM], const float (&rr)[NDIM],
+                                              const float (&t)[NDIM]) const {
+    const float ex = fmaf(rr[kE], t[kE], xs[kE]);
+    const float ey = fmaf(rr[kE + 1], t[kE + 1], xs[kE + 1]);
+    float best = 3.0e38f;
+#pragma unroll
+    for (int i = 0; i < kAgents - 1; ++i) {
+      const float dx = fmaf(rr[3 * i], t[3 * i], xs[3 * i]) - ex;
+      const float dy = fmaf(rr[3 * i + 1], t[3 * i + 1], xs[3 * i + 1]) - ey;
+      best = fminf(best, fmaf(dx, dx, dy * dy));
+    }
+    return sqrt_approx(best);
+  }
   __device__ __forceinline__ float core(const float (&xs)[NDIM], float sigma,
                                         const float (&z)[NDIM]) const {
     const float ex = fmaf(sigma, z[kE], xs[kE]);
@@ -238,6 +275,7 @@ struct PursuitMin {  // g = min_{i < A−1} ‖pos_i − pos_{A−1}‖ − r  (
 // ---------------------------------------------------------------------------------------------
 template <int NDIM>
 struct Linear {  // g = a·y + b (test target; Gaussian-tilt identities)
+  static constexpr bool kHomog = false;
   float a[NDIM];
   float off;
   __device__ explicit Linear(const TargetParams& t) {
@@ -273,6 +311,7 @@ struct Linear {  // g = a·y + b (test target; Gaussian-tilt identities)
 // ---------------------------------------------------------------------------------------------
 template <int NDIM>
 struct Const {  // g = k (test target)
+  static constexpr bool kHomog = false;
   float off;
   __device__ explicit Const(const TargetParams& t) : off(t.np > 0 ? t.p[0] : 0.f) {}
   __device__ __forceinline__ float core(const float (&)[NDIM], float, const float (&)[NDIM]) const {

@@ -15,7 +15,8 @@ is written; DESIGN.md §6 derives each line):
     the minimum any kernel honouring the contract must execute (the C2 kernel's SASS has
     exactly 48 IMAD.WIDE and 53 XOR-LOP3 per 3-block group);
   * Box–Muller per pair: 2 mantissa builds, 1 add, LG2 + SQRT + COS + SIN, 2 multiplies
-    (homogeneous targets — pair union, pursuit-min — 1: the pair's w·r̂ in σ-scaled coordinates);
+    (distance targets — disk, rel-disk-6, pair union, pursuit-min — instead one w·r̂ per
+    (sample, pair) in σ-scaled coordinates);
   * y = x + σ z on the coordinates g reads, g itself, a = A·core + B (1 FFMA), 1 EX2;
   * the moment update: 1 add + n FFMAs.
 Pipe rates (lane-ops per clock per SM) default to the nominal sm_100 figures and are replaced
@@ -55,14 +56,18 @@ def op_counts(n: int, target: str, antithetic: bool = False) -> dict:
     used = G * n                                # normals used per group
     pairs = (used + 1) // 2
     half = used % 2                             # a last pair with only its cos used
-    # targets whose core is homogeneous in the position (pair union, pursuit-min: distances)
-    # need no r̂·cos / r̂·sin products: in σ-scaled coordinates a sample coordinate is one FFMA
-    # x/σ' + r̂·trig (counted with the target below) and the moments take the pair's w·r̂ (one
-    # multiply per pair instead of two)
-    homog = target in ("pair_union", "pursuit_min")
-    fp32_pair = (2 * pairs) if homog else (3 * pairs - half)
+    # targets whose core is a distance (homogeneous of degree 1 in the position: disk,
+    # rel-disk-6, pair union, pursuit-min) need no r̂·cos / r̂·sin products: in σ-scaled
+    # coordinates a sample coordinate is one FFMA x/σ' + r̂·trig (counted with the target below)
+    # and the moments take w·r̂ once per (sample, pair) the sample touches
+    homog = target in ("pair_union", "pursuit_min", "disk", "rel_disk6")
+    if homog:
+        touched = sum((r * n + n - 1) // 2 - (r * n) // 2 + 1 for r in range(G))
+        fp32_draw = pairs + touched
+    else:
+        fp32_draw = 3 * pairs - half
     draw = {"imul": (3 + 15 * Q) / G, "alu": (2 + 17 * Q + 2 * pairs) / G,
-            "fp32": fp32_pair / G, "mufu": (4 * pairs - half) / G}
+            "fp32": fp32_draw / G, "mufu": (4 * pairs - half) / G}
     # ---- per sample: y, g, weight, moments
     samp = {"imul": 0, "alu": 0, "fp32": 0, "mufu": 1}   # EX2
     if target == "quad_bowl":

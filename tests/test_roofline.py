@@ -16,15 +16,18 @@ def test_draw_layout(n, G, Q):
 
 def test_c2_counts_by_hand():
     """n = 3 disk (C2): a group of 4 draws uses 3 Philox blocks → (3 + 15·3)/4 = 12 multiplies,
-    (2 + 17·3 + 2·6)/4 = 16.25 ALU (XORs + 2 mantissa builds per pair, 6 pairs), Box–Muller FP32
-    (3·6)/4 = 4.5 plus the sample's 4 (target) + 1 (FFMA) + 1 (S) + 3 (moments) = 13.5 FP32,
-    MUFU (4·6)/4 + SQRT + EX2 = 8."""
+    (2 + 17·3 + 2·6)/4 = 16.25 ALU (XORs + 2 mantissa builds per pair, 6 pairs). Box–Muller FP32
+    in σ-scaled coordinates: one u per pair (6) and one w·r̂ per (sample, pair) — the 12 normals
+    0-1-2 | 3-4-5 | 6-7-8 | 9-10-11 split the pairs (0,1)(2,3)(4,5)(6,7)(8,9)(10,11) as
+    {(0,1),(2,3)}, {(2,3),(4,5)}, {(6,7),(8,9)}, {(8,9),(10,11)}: 8 — so (6 + 8)/4 = 3.5, plus the
+    sample's 4 (target) + 1 (FFMA) + 1 (S) + 3 (moments) = 12.5 FP32; MUFU (4·6)/4 + SQRT + EX2
+    = 8."""
     ops = RL.op_counts(3, "disk")
     assert ops["imul"] == 12.0
     assert ops["alu"] == 16.25
-    assert ops["fp32"] == 13.5
+    assert ops["fp32"] == 12.5
     assert ops["mufu"] == 8.0
-    assert ops["issue"] == 49.75
+    assert ops["issue"] == 48.75
 
 
 def test_c5_counts_by_hand():
