@@ -56,6 +56,11 @@ VARIANTS = {
 # shuffles (bit-identical, 4 IMAD.WIDE fewer per lane per two samples) 4531 vs 4450 ms; the
 # dual loop unrolled x2 / x4 4504 / 4619 vs 4454 ms; 2-lane groups 4473 vs 4455 ms; the
 # per-thread layout at 128 registers (spilling) 4873 vs 4458 ms.
+# Late round 2, after the sigma-scaled lane-group pass (4370 ms on the same queries): one
+# single-sample trip first in warps 4-7 so their dual trips run half a trip out of phase with
+# warps 0-3 (the loop is phased: Philox-only, then MUFU-heavy, then FP32), bit-identical:
+# 4478 ms (+2.5 %), removed; single-sample trips at 3 / 4 CTAs per SM 4404 / 4392 ms, the dual
+# loop at 3 CTAs per SM (spilling) 4624 ms.
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
