@@ -40,6 +40,17 @@ VARIANTS = {
     # dfHi 4836, dfLo 4969, dfA 5310; profiles/r2_philox_dfma_variants.jsonl)
     # lane-group speculative kernel at 2 CTAs/SM (128 registers) instead of 3
     "spec2": ["-DHJMC_LG_SPEC_MINB=2"],
+    # the scheduling tie of the lane-group dual loop (default: on, at radius 0, loop unrolled x2).
+    # C5, 1,184 queries: default 4326 ms; no tie (unrolled x2) 4361; tie at radius 1/2/3/5
+    # 4379/4406/4412/4417; tie without unrolling 4380, with x4 4395; the tie also from each trip
+    # to the next (loop-carried) 4397; a tie between every pair of consecutive Philox blocks
+    # 4886 (x2: 4810); four samples per trip with one SQRT + EX2 per lane per four samples
+    # (reduce-scatter of the minima; removed) 4386 ms
+    "nochain": ["-DHJMC_LG_CHAIN=0"],
+    "at1": ["-DHJMC_LG_CHAIN_AT=1"],
+    "at2": ["-DHJMC_LG_CHAIN_AT=2"],
+    "at3": ["-DHJMC_LG_CHAIN_AT=3"],
+    "at5": ["-DHJMC_LG_CHAIN_AT=5"],
     "dfA": ["-DHJMC_PHILOX_DFMA_MASK=0xFFFFFu"],
     "df5": ["-DHJMC_PHILOX_DFMA_MASK=0x55555u"],
     "dfA5": ["-DHJMC_PHILOX_DFMA_MASK=0xAAAAAu"],
