@@ -245,23 +245,23 @@ __device__ float mc_max_exponent(const Tgt& tgt, const float (&xs)[NDIM], float 
         if (antithetic && 2 * q + 1 < N) amax = fmaxf(amax, A * tgt.core_polar(xs, rn, t));
       }
     }
-    return amax;
-  }
-  for (uint32_t g = tid; g < groups; g += NT) {
-    float zz[L::L];
-    group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
+  } else {
+    for (uint32_t g = tid; g < groups; g += NT) {
+      float zz[L::L];
+      group_normals_hat<NDIM>(zz, g, w1base, qid, tag, rk);
 #pragma unroll
-    for (int r = 0; r < L::G; ++r) {
-      const uint32_t q = g * L::G + r;
-      if (q >= draws) continue;
-      float z[NDIM];
+      for (int r = 0; r < L::G; ++r) {
+        const uint32_t q = g * L::G + r;
+        if (q >= draws) continue;
+        float z[NDIM];
 #pragma unroll
-      for (int d = 0; d < NDIM; ++d) z[d] = zz[r * NDIM + d];
-      float t = 0.f;  // tilt term (zero for the plain proposal)
+        for (int d = 0; d < NDIM; ++d) z[d] = zz[r * NDIM + d];
+        float t = 0.f;  // tilt term (zero for the plain proposal)
 #pragma unroll
-      for (int d = 0; d < NDIM; ++d) t = fmaf(tz[d], z[d], t);
-      amax = fmaxf(amax, fmaf(A, tgt.core(xs, sigma, z), t));
-      if (antithetic && 2 * q + 1 < N) amax = fmaxf(amax, fmaf(A, tgt.core(xs, -sigma, z), -t));
+        for (int d = 0; d < NDIM; ++d) t = fmaf(tz[d], z[d], t);
+        amax = fmaxf(amax, fmaf(A, tgt.core(xs, sigma, z), t));
+        if (antithetic && 2 * q + 1 < N) amax = fmaxf(amax, fmaf(A, tgt.core(xs, -sigma, z), -t));
+      }
     }
   }
   return amax;
