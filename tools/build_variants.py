@@ -72,6 +72,14 @@ VARIANTS = {
 # warps 0-3 (the loop is phased: Philox-only, then MUFU-heavy, then FP32), bit-identical:
 # 4478 ms (+2.5 %), removed; single-sample trips at 3 / 4 CTAs per SM 4404 / 4392 ms, the dual
 # loop at 3 CTAs per SM (spilling) 4624 ms.
+# Re-entry of round 2 (HEAD kernel, 4325 ms on the same queries): cos/sin of the lane-group draws
+# from a 4,096-entry shared-memory (cos, sin) table at the top 12 angle bits plus a first-order
+# rotation by the remaining 11 bits (error <= 2.9e-7, MUFU.SIN/COS's own size; all 127 GPU tests
+# passed with it) instead of FMUL + FMUL.RZ + MUFU.COS + MUFU.SIN: 7 instructions per pair (SHF,
+# LEA, LDS.64, LOP3, 3 FFMA) for 5, MUFU 100 -> 52 per eval, loop 803 -> 856 instructions per four
+# lane-samples: 4520 ms (+4.5 %); the paper's 45-D preset 10.12 -> 10.48 ms. Halving the MUFU
+# load does not pay for 6 % more issue slots and the FFMAs that land on the FMA-heavy pipe:
+# the loop is bound by issue and the FMA-heavy pipe (IMAD.WIDE), not by the XU pipe. Removed.
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
