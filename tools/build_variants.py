@@ -51,6 +51,15 @@ VARIANTS = {
     "at2": ["-DHJMC_LG_CHAIN_AT=2"],
     "at3": ["-DHJMC_LG_CHAIN_AT=3"],
     "at5": ["-DHJMC_LG_CHAIN_AT=5"],
+    # CTA size / occupancy of the lane-group dual loop (C5, 1,184 queries; default 256 threads x 2
+    # CTAs at 128 registers = 16 warps/SM: 4327 ms): 128 threads x 4 CTAs at 128 registers (16
+    # warps) 4404 ms; 128 threads x 5 CTAs at 96 registers (20 warps, no spill inside the loop)
+    # 4488 ms; 256 threads x 1 CTA at 170 registers (8 warps) 4709 ms. 512 threads does not build
+    # (the warp-per-unit instantiation's shared memory).
+    "nt128mb5": ["-DHJMC_NT=128", "-DHJMC_MINB=5"],
+    "nt128mb4": ["-DHJMC_NT=128", "-DHJMC_MINB=4"],
+    "nt512mb1": ["-DHJMC_NT=512", "-DHJMC_MINB=1"],
+    "nt256mb1": ["-DHJMC_NT=256", "-DHJMC_MINB=1"],
     "dfA": ["-DHJMC_PHILOX_DFMA_MASK=0xFFFFFu"],
     "df5": ["-DHJMC_PHILOX_DFMA_MASK=0x55555u"],
     "dfA5": ["-DHJMC_PHILOX_DFMA_MASK=0xAAAAAu"],
