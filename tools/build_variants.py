@@ -58,6 +58,8 @@ VARIANTS = {
     # (the warp-per-unit instantiation's shared memory).
     "nt128mb5": ["-DHJMC_NT=128", "-DHJMC_MINB=5"],
     "nt128mb4": ["-DHJMC_NT=128", "-DHJMC_MINB=4"],
+    # (-Xptxas -O2 and --allow-expensive-optimizations=false give byte-identical SASS for the
+    # lane-group kernel: nothing to measure)
     "nt512mb1": ["-DHJMC_NT=512", "-DHJMC_MINB=1"],
     "nt256mb1": ["-DHJMC_NT=256", "-DHJMC_MINB=1"],
     "dfA": ["-DHJMC_PHILOX_DFMA_MASK=0xFFFFFu"],
