@@ -55,6 +55,12 @@ if __name__ == "__main__":
             row["bit_identical"] = bool(torch.equal(out["v"], outf["v"]) and torch.equal(out["tube"], outf["tube"]))
         rows.append(row)
         print(json.dumps(row), flush=True)
+    full_rows = [r for r in rows if "full_s" in r]
     print(json.dumps({"config": p.name, "slices": len(p.slices), "queries": p.M,
                       "total_fast_s_1gpu": round(total_fast, 1),
+                      "full_schedule_slices_measured": len(full_rows),
+                      "total_full_s_1gpu": round(sum(r["full_s"] for r in full_rows), 1),
+                      "evals_per_s_full": (len(full_rows) * per * p.N * p.K * p.Kp
+                                           / max(sum(r["full_s"] for r in full_rows), 1e-9)),
+                      "all_bit_identical": all(r["bit_identical"] for r in full_rows),
                       "evals_full_schedule": p.M * p.N * p.K * p.Kp}))
