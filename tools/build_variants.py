@@ -60,6 +60,15 @@ VARIANTS = {
     "nt128mb4": ["-DHJMC_NT=128", "-DHJMC_MINB=4"],
     # (-Xptxas -O2 and --allow-expensive-optimizations=false give byte-identical SASS for the
     # lane-group kernel: nothing to measure)
+    # ptxas --register-usage-level 0 / 10 (default 5): C5 4388 / 4435 ms vs 4330; C4 2470 / 2418
+    # vs 2415 ms — schedule-level differences move the loop by 1-2 %
+    "rul0": ["-Xptxas", "--register-usage-level=0"],
+    "rul10": ["-Xptxas", "--register-usage-level=10"],
+    # (measured and removed: source-order permutations of the lane-group trip — Philox blocks,
+    # moment pairs and partial-min triples each ascending or descending, 7 combinations, all
+    # bit-identical, every one a different ptxas schedule of the same 803 instructions: 4350,
+    # 4365, 4442, 4350, 4407, 4362, 4410 ms vs the default order's 4328 ms. Schedules of this
+    # loop spread over ~2.6 %, and the default is the best of the sampled ones.)
     "nt512mb1": ["-DHJMC_NT=512", "-DHJMC_MINB=1"],
     "nt256mb1": ["-DHJMC_NT=256", "-DHJMC_MINB=1"],
     "dfA": ["-DHJMC_PHILOX_DFMA_MASK=0xFFFFFu"],
